@@ -1,0 +1,217 @@
+"""CPU oracle for the reproducible GroupBy-SUM of arxiv 1802.09883.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s cpu_baseline / ``--impl reference`` leg may import this
+package.  It loads ``oracle/liboracle.so`` (built from ``repro_oracle.c`` by
+:func:`build`), which shares no code with the CUDA path.
+
+Every function maps one-to-one onto a C function of ``repro_oracle.c``; the
+paper passages each one follows are cited there (Alg. 1 PAPER.md:654-687,
+Eq. 1, merge SPEC.md:186-195, GroupBy PAPER.md:291-302).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "repro_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+OK, EINVAL, EKEY, EDOM, ERANGE, ENOMEM = 0, -1, -2, -3, -4, -6
+KIND_F64, KIND_F32, KIND_TOY = 0, 1, 2
+F32, F64 = 0, 1  # dtype codes (same numbering as the C-ABI, defined separately)
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc -O2 -ffp-contract=off (no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+               "-pthread", "-o", _LIB, _SRC, "-lm"]
+        subprocess.run(cmd, check=True)
+    return _LIB
+
+
+class Params(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("m", ctypes.c_int), ("W", ctypes.c_int),
+                ("f", ctypes.c_int), ("L", ctypes.c_int), ("emin", ctypes.c_int),
+                ("emax", ctypes.c_int), ("ties_away", ctypes.c_int),
+                ("thr_shift", ctypes.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        d, P, dp = ctypes.c_double, ctypes.POINTER(Params), ctypes.POINTER(ctypes.c_double)
+        L.orc_ufp.argtypes, L.orc_ufp.restype = [d], d
+        L.orc_ulp.argtypes, L.orc_ulp.restype = [P, d], d
+        L.orc_lsb_force.argtypes, L.orc_lsb_force.restype = [P, d], d
+        L.orc_eft.argtypes, L.orc_eft.restype = [P, d, d, dp, dp], None
+        L.orc_fadd.argtypes, L.orc_fadd.restype = [P, d, d], d
+        L.orc_round.argtypes, L.orc_round.restype = [P, d], d
+        L.orc_init.argtypes, L.orc_init.restype = [P, dp, dp], ctypes.c_int
+        L.orc_deposit.argtypes, L.orc_deposit.restype = [P, dp, dp, d], ctypes.c_int
+        L.orc_merge.argtypes, L.orc_merge.restype = [P, dp, dp, dp, dp], ctypes.c_int
+        L.orc_finalize.argtypes, L.orc_finalize.restype = [P, dp, dp, dp], ctypes.c_int
+        L.orc_carry.argtypes, L.orc_carry.restype = [P, dp, dp], None
+        L.orc_params_for.argtypes, L.orc_params_for.restype = [P, ctypes.c_int, ctypes.c_int], ctypes.c_int
+        vp = ctypes.c_void_p
+        L.orc_groupby_sum.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                      ctypes.c_int32, vp, vp, ctypes.c_int, ctypes.c_int]
+        L.orc_groupby_sum.restype = ctypes.c_int
+        L.orc_groupby_sum_select.argtypes = [vp, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                             ctypes.c_int32, vp, ctypes.c_int32, vp, vp, ctypes.c_int]
+        L.orc_groupby_sum_select.restype = ctypes.c_int
+        L.orc_plain_sum.argtypes, L.orc_plain_sum.restype = [P, vp, ctypes.c_int64], d
+        _lib = L
+    return _lib
+
+
+def params(dtype: int | None = None, K: int = 3, *, m: int | None = None, W: int | None = None,
+           f: int = 0, emin: int = -1022, emax: int = 1023, ties_away: bool = True,
+           thr_shift: int | None = None) -> Params:
+    """Production parameters (dtype given) or a toy format (m, W given)."""
+    p = Params()
+    if dtype is not None:
+        st = lib().orc_params_for(ctypes.byref(p), dtype, K)
+        assert st == OK
+    else:
+        p.kind, p.m, p.W, p.L, p.emin, p.emax = KIND_TOY, m, W, K, emin, emax
+    p.f = f if dtype is None else p.f
+    p.ties_away = 1 if ties_away else 0
+    p.thr_shift = (p.W - 1) if thr_shift is None else thr_shift
+    return p
+
+
+@dataclass
+class State:
+    """<S, C> of one reproducible accumulator."""
+    S: list
+    C: list
+
+    def key(self):
+        return tuple(np.float64(x).view(np.uint64).item() for x in self.S + self.C)
+
+
+def _arr(vals):
+    return (ctypes.c_double * len(vals))(*vals)
+
+
+def init(p: Params) -> State:
+    S, C = (ctypes.c_double * p.L)(), (ctypes.c_double * p.L)()
+    assert lib().orc_init(ctypes.byref(p), S, C) == OK
+    return State(list(S), list(C))
+
+
+def deposit(p: Params, st: State, b: float) -> int:
+    S, C = _arr(st.S), _arr(st.C)
+    rc = lib().orc_deposit(ctypes.byref(p), S, C, float(b))
+    st.S, st.C = list(S), list(C)
+    return rc
+
+
+def deposit_all(p: Params, values, st: State | None = None) -> State:
+    st = init(p) if st is None else st
+    for b in values:
+        rc = deposit(p, st, b)
+        if rc != OK:
+            raise ValueError(f"deposit failed: {rc}")
+    return st
+
+
+def merge(p: Params, dst: State, src: State) -> int:
+    S, C = _arr(dst.S), _arr(dst.C)
+    rc = lib().orc_merge(ctypes.byref(p), S, C, _arr(src.S), _arr(src.C))
+    dst.S, dst.C = list(S), list(C)
+    return rc
+
+
+def finalize(p: Params, st: State) -> float:
+    q = ctypes.c_double()
+    rc = lib().orc_finalize(ctypes.byref(p), _arr(st.S), _arr(st.C), ctypes.byref(q))
+    if rc != OK:
+        raise ValueError(f"finalize failed: {rc}")
+    return q.value
+
+
+def carry(p: Params, S: float, C: float):
+    s, c = ctypes.c_double(S), ctypes.c_double(C)
+    lib().orc_carry(ctypes.byref(p), ctypes.byref(s), ctypes.byref(c))
+    return s.value, c.value
+
+
+def eft(p: Params, a: float, b: float):
+    q, r = ctypes.c_double(), ctypes.c_double()
+    lib().orc_eft(ctypes.byref(p), a, b, ctypes.byref(q), ctypes.byref(r))
+    return q.value, r.value
+
+
+def ufp(x: float) -> float:
+    return lib().orc_ufp(x)
+
+
+def ulp(p: Params, x: float) -> float:
+    return lib().orc_ulp(ctypes.byref(p), x)
+
+
+def lsb_force(p: Params, x: float) -> float:
+    return lib().orc_lsb_force(ctypes.byref(p), x)
+
+
+def fadd(p: Params, a: float, b: float) -> float:
+    return lib().orc_fadd(ctypes.byref(p), a, b)
+
+
+def fround(p: Params, x: float) -> float:
+    return lib().orc_round(ctypes.byref(p), x)
+
+
+def plain_sum(p: Params, values) -> float:
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    return lib().orc_plain_sum(ctypes.byref(p), v.ctypes.data, v.size)
+
+
+def default_threads() -> int:
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def groupby_sum(keys: np.ndarray, vals: np.ndarray, n_groups: int, fold: int, *,
+                threads: int | None = None, mode: int = 0, with_state: bool = False):
+    """GroupBy-SUM (O5/O6).  Returns (status, out[, state]); state is
+    [n_groups, 2K] float64 rows S[0..K) then C[0..K) (SPEC.md:277 layout)."""
+    keys = np.ascontiguousarray(keys, dtype=np.int32)
+    dtype = F64 if vals.dtype == np.float64 else F32
+    vals = np.ascontiguousarray(vals)
+    assert vals.dtype in (np.float64, np.float32)
+    out = np.zeros(n_groups, dtype=vals.dtype)
+    state = np.zeros((n_groups, 2 * fold), dtype=np.float64) if with_state else None
+    rc = lib().orc_groupby_sum(keys.ctypes.data, vals.ctypes.data, keys.size, n_groups, fold,
+                               dtype, out.ctypes.data,
+                               state.ctypes.data if with_state else None,
+                               threads or default_threads(), mode)
+    return (rc, out, state) if with_state else (rc, out)
+
+
+def groupby_sum_select(keys: np.ndarray, vals: np.ndarray, n_groups: int, fold: int,
+                       sel: np.ndarray, *, threads: int | None = None, with_state: bool = False):
+    """GroupBy-SUM restricted to the groups in ``sel`` (outputs indexed like sel)."""
+    keys = np.ascontiguousarray(keys, dtype=np.int32)
+    sel = np.ascontiguousarray(sel, dtype=np.int32)
+    dtype = F64 if vals.dtype == np.float64 else F32
+    vals = np.ascontiguousarray(vals)
+    out = np.zeros(sel.size, dtype=vals.dtype)
+    state = np.zeros((sel.size, 2 * fold), dtype=np.float64) if with_state else None
+    rc = lib().orc_groupby_sum_select(keys.ctypes.data, vals.ctypes.data, keys.size, n_groups,
+                                      fold, dtype, sel.ctypes.data, sel.size, out.ctypes.data,
+                                      state.ctypes.data if with_state else None,
+                                      threads or default_threads())
+    return (rc, out, state) if with_state else (rc, out)
