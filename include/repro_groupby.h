@@ -1,0 +1,216 @@
+/*
+ * repro_groupby.h -- C-ABI of the B200-native reproducible GroupBy-SUM
+ * (arxiv 1802.09883, "Reproducible Floating-Point Aggregation in RDBMSs").
+ *
+ * The operation (Section 2.1): turn a sequence of
+ * <key, value> pairs into <key, aggregate> pairs, where the aggregate of a
+ * group is the sum of its values, with "exactly the same bit pattern for any
+ * execution".  Each group's sum is the paper's repro<ScalarT, L> accumulator
+ * with L = `fold` levels: Algorithm 1
+ * deposits, operator+=(repro) merges,
+ * Eq. 1 reads out.  Readings where the paper is silent
+ * (ties away from zero, threshold 2^(W-1) ulp, f = 0, W = 40 / 18) are listed
+ * in DESIGN.md; the result bits equal those of the CPU oracle in oracle/.
+ *
+ * Conventions shared by every entry point
+ *   - Array arguments are CUDA DEVICE pointers owned by the caller, unless the
+ *     name ends in _host.  Keys are int32, dense in [0, n_groups) (identity
+ *     hashing).  Values are binary32 (dtype REPRO_F32) or
+ *     binary64 (REPRO_F64); `out` has n_groups elements of the same type.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *   - Blocking calls return after the stream has been synchronised and report
+ *     device-detected errors.  _async calls only enqueue work; their device
+ *     status word (int32, device memory, caller owned) receives the status.
+ *   - Argument errors (REPRO_EINVAL) are reported before anything is
+ *     launched: n < 0, n_groups < 1, fold not in [1, 4],
+ *     unknown dtype, NULL pointer with n > 0, mismatched accumulators.
+ *   - Device-detected errors have a fixed precedence that does not depend on
+ *     row order: REPRO_EKEY (key outside [0, n_groups)) > REPRO_EDOM (NaN or
+ *     Inf value) > REPRO_ERANGE (|value| >= 2^987 for binary64 / 2^120 for
+ *     binary32, where the top extractor would overflow; or a binary32 carry
+ *     count |C| >= 2^24 at read-out).  Output contents are unspecified on
+ *     error.
+ *   - Empty groups and exactly cancelling groups read out as +0.0.
+ *   - Guarantee: `out` bits depend only on the multiset of (key, value)
+ *     pairs, fold and dtype -- not on row order, chunking into deposits,
+ *     merge order, launch configuration or GPU count.
+ */
+#ifndef REPRO_GROUPBY_H
+#define REPRO_GROUPBY_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* dtype */
+#define REPRO_F32 0 /* binary32: m = 23, W = 18 */
+#define REPRO_F64 1 /* binary64: m = 52, W = 40                     */
+
+/* status codes */
+#define REPRO_OK 0
+#define REPRO_EINVAL (-1)
+#define REPRO_EKEY (-2)
+#define REPRO_EDOM (-3)
+#define REPRO_ERANGE (-4)
+#define REPRO_ECUDA (-5)
+#define REPRO_ENOMEM (-6)
+
+/* Human-readable name of a status code (static string). */
+const char *repro_strerror(int status);
+
+/* Library build/version string (static). */
+const char *repro_version(void);
+
+/* ------------------------------------------------------------------------
+ * One-shot GroupBy-SUM
+ * ---------------------------------------------------------------------- */
+
+/* out[g] = reproducible sum of vals[i] over rows with keys[i] == g,
+ * for g in [0, n_groups).  keys: int32[n]; vals: dtype[n]; out: dtype[n_groups].
+ * Blocking; scratch memory comes from a library-internal cache (grown on
+ * demand, freed by repro_release_cache). */
+int repro_groupby_sum(const int32_t *keys, const void *vals, int64_t n,
+                      int32_t n_groups, int32_t fold, int32_t dtype, void *out);
+
+/* Bytes of device workspace repro_groupby_sum_async needs for this shape. */
+size_t repro_groupby_workspace_bytes(int64_t n, int32_t n_groups, int32_t fold,
+                                     int32_t dtype);
+
+/* Enqueue the GroupBy-SUM on `stream` using the caller's workspace
+ * (>= repro_groupby_workspace_bytes, 256-byte aligned).  d_status: int32 in
+ * device memory, overwritten with the REPRO_* status when the work completes.
+ * Returns REPRO_EINVAL / REPRO_ENOMEM (workspace too small) / REPRO_ECUDA at
+ * enqueue time, else REPRO_OK. */
+int repro_groupby_sum_async(const int32_t *keys, const void *vals, int64_t n,
+                            int32_t n_groups, int32_t fold, int32_t dtype,
+                            void *out, void *workspace, size_t ws_bytes,
+                            void *stream, int32_t *d_status);
+
+/* Same result from HOST arrays (pageable or pinned): the library copies the
+ * rows to the device in pipelined chunks overlapped with the deposit
+ * kernels, and copies out[n_groups] back.  Blocking. */
+int repro_groupby_sum_host(const int32_t *keys_host, const void *vals_host,
+                           int64_t n, int32_t n_groups, int32_t fold,
+                           int32_t dtype, void *out_host);
+
+/* Free the internal workspace cache of the blocking entry points. */
+void repro_release_cache(void);
+
+/* ------------------------------------------------------------------------
+ * Accumulator handles: n_groups device-resident repro<ScalarT, fold> states
+ * (the paper's intermediate aggregates).  A handle is not
+ * thread-safe; distinct handles are independent.  All calls are blocking.
+ * ---------------------------------------------------------------------- */
+typedef struct repro_acc repro_acc;
+
+/* New handle with every group at the initial state (O1). */
+int repro_acc_create(repro_acc **acc, int32_t n_groups, int32_t fold,
+                     int32_t dtype);
+
+/* Deposit n rows (device arrays) into the handle (Alg. 1 per row). */
+int repro_acc_deposit(repro_acc *acc, const int32_t *keys, const void *vals,
+                      int64_t n);
+
+/* dst += src (operator+=(repro)); same shape required. */
+int repro_acc_merge(repro_acc *dst, const repro_acc *src);
+
+/* out[g] = Eq. 1 read-out of every group (device array); non-mutating. */
+int repro_acc_finalize(const repro_acc *acc, void *out);
+
+/* Serialised state: per group S[0..fold) then C[0..fold) in
+ * the native width (double for F64, float for F32), little-endian; device
+ * array of n_groups * 2 * fold elements.  Non-mutating. */
+int repro_acc_export(const repro_acc *acc, void *state);
+
+/* Replace the handle's state by a serialised one (REPRO_EINVAL if any group
+ * is not a canonical state: S off the W-lattice, S outside [1.5, 1.75) ufp,
+ * C not an integer). */
+int repro_acc_import(repro_acc *acc, const void *state);
+
+/* Reset every group to the initial state. */
+int repro_acc_reset(repro_acc *acc);
+
+void repro_acc_destroy(repro_acc *acc);
+
+/* Shape queries. */
+int32_t repro_acc_n_groups(const repro_acc *acc);
+int32_t repro_acc_fold(const repro_acc *acc);
+int32_t repro_acc_dtype(const repro_acc *acc);
+
+/* ------------------------------------------------------------------------
+ * Multi-GPU exchange (one process per GPU; the caller runs the collectives,
+ * e.g. NCCL through torch.distributed).  Integer-only, so the result does
+ * not depend on the collective's reduction order:
+ *   1. repro_acc_top_levels(acc, k)          k: int32[n_groups] device
+ *   2. all-reduce MAX over ranks on k
+ *   3. repro_acc_window_export(acc, k, limbs) limbs: int64[n_groups*fold*2]
+ *      (the group's level sums realigned to the global top k[g] -- the
+ *      paper's level demotion, PAPER.md:660-665 -- as carry-split limbs
+ *      lo in [0, 2^32), hi = floor(T / 2^32))
+ *   4. all-reduce (or reduce-scatter by group range) SUM on limbs
+ *   5. repro_acc_window_import(acc, k, limbs) (canonicalises, Alg. 1
+ *      lines 17-21)
+ * The result is bit-identical to depositing every rank's rows into one
+ * handle.
+ * ---------------------------------------------------------------------- */
+int repro_acc_top_levels(const repro_acc *acc, int32_t *k_out);
+int repro_acc_window_export(const repro_acc *acc, const int32_t *k_global,
+                            int64_t *limbs_out);
+int repro_acc_window_import(repro_acc *acc, const int32_t *k_global,
+                            const int64_t *limbs);
+/* Range form of window_import for a reduce-scatter by contiguous group
+ * range: groups [g0, g0 + count) of the handle take the given limbs
+ * (int64[count*fold*2]); k_global is int32[count] for that range. */
+int repro_acc_window_import_range(repro_acc *acc, int32_t g0, int32_t count,
+                                  const int32_t *k_global,
+                                  const int64_t *limbs);
+
+/* ------------------------------------------------------------------------
+ * Non-reproducible baseline on the same GPU (BASELINE.json north_star):
+ * out[g] = atomicAdd-accumulated sum in the value dtype (or in binary64 when
+ * accumulate_f64 != 0 and dtype is F32).  variant 0: one global atomicAdd
+ * per row; variant 1: shared-memory privatised table per block (compare-
+ * and-swap on sm_100a) flushed with global atomics.  out is zeroed inside.
+ * Stream-ordered, non-blocking; returns REPRO_EINVAL for bad arguments or
+ * when variant 1 does not fit shared memory.
+ * ---------------------------------------------------------------------- */
+int repro_baseline_atomic_sum(const int32_t *keys, const void *vals, int64_t n,
+                              int32_t n_groups, int32_t dtype, int32_t variant,
+                              int32_t accumulate_f64, void *out, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Introspection for tests and the benchmark.
+ * ---------------------------------------------------------------------- */
+/* Number of kernels the last call on this host thread enqueued. */
+int32_t repro_last_launch_count(void);
+/* Path the last GroupBy call on this host thread took: 0 = on-chip tables,
+ * 1 = radix-partitioned, -1 = none. */
+int32_t repro_last_path(void);
+/* Largest n_groups the on-chip path handles for (fold, dtype). */
+int32_t repro_onchip_max_groups(int32_t fold, int32_t dtype);
+/* Force a path for testing: -1 auto (default), 0 on-chip, 1 partitioned.
+ * Never changes result bits. */
+void repro_set_path_override(int32_t path);
+
+/* Choose the on-chip accumulate kernel for testing: 0 auto (default), 1 the
+ * per-row shared-atomic kernel, 2 the tile-sorted kernel.  Never changes
+ * result bits. */
+void repro_set_kernel_variant(int32_t variant);
+
+/* Per-kernel device timing (benchmark aid).  While enabled, every kernel the
+ * library enqueues from this host thread is bracketed by a CUDA event pair
+ * recorded on the launching stream. */
+void repro_timing_enable(int32_t on);
+/* Synchronises on the recorded events and returns, for up to `max` distinct
+ * kernels, their names (static strings), launch counts and summed device
+ * milliseconds; clears the records.  Returns the number of kernels. */
+int32_t repro_timing_collect(const char **names, int32_t *counts, double *total_ms, int32_t max);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* REPRO_GROUPBY_H */

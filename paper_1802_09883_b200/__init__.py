@@ -1,0 +1,319 @@
+"""B200-native reproducible GroupBy-SUM (arxiv 1802.09883).
+
+Thin ctypes binding over the C-ABI of ``include/repro_groupby.h``
+(``_lib/librepro_b200.so``, hand-written sm_100a kernels).  Every function
+here only marshals arguments: torch tensors are passed as device pointers and
+every step of the GroupBy runs in the library's kernels.  There is no CPU
+fallback: importing the package fails loudly when the library is missing.
+
+Entry points mirror the C names:
+  groupby_sum / groupby_sum_async / groupby_sum_host / workspace_bytes
+  Accumulator (repro_acc_*), baseline_atomic_sum, and introspection helpers.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .build_native import LIB as _LIB_PATH
+
+F32, F64 = 0, 1
+OK, EINVAL, EKEY, EDOM, ERANGE, ECUDA, ENOMEM = 0, -1, -2, -3, -4, -5, -6
+_STATUS = {0: "OK", -1: "EINVAL", -2: "EKEY", -3: "EDOM", -4: "ERANGE", -5: "ECUDA", -6: "ENOMEM"}
+
+if not os.path.exists(_LIB_PATH):
+    raise ImportError(
+        f"librepro_b200.so not found at {_LIB_PATH}: build it with "
+        "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
+
+_lib = ctypes.CDLL(_LIB_PATH)
+LIB_PATH = _LIB_PATH
+
+_vp, _i32, _i64, _sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+
+
+def _sig(name, res, *args):
+    f = getattr(_lib, name)
+    f.restype = res
+    f.argtypes = list(args)
+    return f
+
+
+_sig("repro_strerror", ctypes.c_char_p, ctypes.c_int)
+_sig("repro_version", ctypes.c_char_p)
+_sig("repro_groupby_sum", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp)
+_sig("repro_groupby_workspace_bytes", _sz, _i64, _i32, _i32, _i32)
+_sig("repro_groupby_sum_async", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp)
+_sig("repro_groupby_sum_host", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp)
+_sig("repro_release_cache", None)
+_sig("repro_acc_create", ctypes.c_int, ctypes.POINTER(_vp), _i32, _i32, _i32)
+_sig("repro_acc_deposit", ctypes.c_int, _vp, _vp, _vp, _i64)
+_sig("repro_acc_merge", ctypes.c_int, _vp, _vp)
+_sig("repro_acc_finalize", ctypes.c_int, _vp, _vp)
+_sig("repro_acc_export", ctypes.c_int, _vp, _vp)
+_sig("repro_acc_import", ctypes.c_int, _vp, _vp)
+_sig("repro_acc_reset", ctypes.c_int, _vp)
+_sig("repro_acc_destroy", None, _vp)
+_sig("repro_acc_n_groups", _i32, _vp)
+_sig("repro_acc_fold", _i32, _vp)
+_sig("repro_acc_dtype", _i32, _vp)
+_sig("repro_acc_top_levels", ctypes.c_int, _vp, _vp)
+_sig("repro_acc_window_export", ctypes.c_int, _vp, _vp, _vp)
+_sig("repro_acc_window_import", ctypes.c_int, _vp, _vp, _vp)
+_sig("repro_acc_window_import_range", ctypes.c_int, _vp, _i32, _i32, _vp, _vp)
+_sig("repro_baseline_atomic_sum", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp)
+_sig("repro_last_launch_count", _i32)
+_sig("repro_last_path", _i32)
+_sig("repro_onchip_max_groups", _i32, _i32, _i32)
+_sig("repro_set_path_override", None, _i32)
+_sig("repro_set_kernel_variant", None, _i32)
+_sig("repro_timing_enable", None, _i32)
+_sig("repro_timing_collect", _i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_i32),
+     ctypes.POINTER(ctypes.c_double), _i32)
+
+
+class ReproError(RuntimeError):
+    def __init__(self, status: int, what: str = ""):
+        self.status = status
+        msg = _lib.repro_strerror(status).decode()
+        super().__init__(f"{what}: {_STATUS.get(status, status)} ({msg})")
+
+
+def _check(status: int, what: str):
+    if status != OK:
+        raise ReproError(status, what)
+
+
+def version() -> str:
+    return _lib.repro_version().decode()
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float64:
+        return F64
+    if t.dtype == torch.float32:
+        return F32
+    raise TypeError(f"values must be float32 or float64, got {t.dtype}")
+
+
+def _dev(t, name, dtype=None):
+    torch = _torch()
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    return t.data_ptr() if t.numel() else None
+
+
+def _stream_ptr(stream):
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def groupby_sum(keys, vals, n_groups: int, fold: int = 3, out=None):
+    """Reproducible GroupBy-SUM (blocking).  keys int32[n], vals f32/f64[n] on CUDA."""
+    torch = _torch()
+    dt = _dtype_code(vals)
+    if keys.numel() != vals.numel():
+        raise ValueError("keys and vals differ in length")
+    if out is None:
+        out = torch.empty(n_groups, dtype=vals.dtype, device=vals.device)
+    st = _lib.repro_groupby_sum(_dev(keys, "keys", torch.int32), _dev(vals, "vals"), keys.numel(),
+                                n_groups, fold, dt, _dev(out, "out", vals.dtype))
+    _check(st, "repro_groupby_sum")
+    return out
+
+
+def workspace_bytes(n: int, n_groups: int, fold: int, dtype: int) -> int:
+    return _lib.repro_groupby_workspace_bytes(n, n_groups, fold, dtype)
+
+
+def make_workspace(n: int, n_groups: int, fold: int, dtype: int, device="cuda"):
+    torch = _torch()
+    nbytes = workspace_bytes(n, n_groups, fold, dtype)
+    if nbytes == 0:
+        raise ReproError(EINVAL, "repro_groupby_workspace_bytes")
+    return torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+
+
+def _aligned_ptr(ws):
+    p = ws.data_ptr()
+    return (p + 255) // 256 * 256, ws.numel() - ((p + 255) // 256 * 256 - p)
+
+
+def groupby_sum_async(keys, vals, n_groups: int, fold: int, out, workspace, status, stream=None):
+    """Enqueue the GroupBy on `stream` (default: current) with a caller
+    workspace (make_workspace) and an int32 device status word."""
+    torch = _torch()
+    dt = _dtype_code(vals)
+    wp, wb = _aligned_ptr(workspace)
+    st = _lib.repro_groupby_sum_async(_dev(keys, "keys", torch.int32), _dev(vals, "vals"), keys.numel(), n_groups,
+                                      fold, dt, _dev(out, "out", vals.dtype), wp, wb, _stream_ptr(stream),
+                                      _dev(status, "status", torch.int32))
+    _check(st, "repro_groupby_sum_async")
+
+
+def groupby_sum_host(keys, vals, n_groups: int, fold: int = 3, out=None):
+    """GroupBy from HOST (CPU, ideally pinned) tensors; returns a CPU tensor."""
+    torch = _torch()
+    if keys.is_cuda or vals.is_cuda:
+        raise TypeError("groupby_sum_host takes host tensors")
+    keys = keys.contiguous()
+    vals = vals.contiguous()
+    if keys.dtype != torch.int32:
+        raise TypeError("keys must be int32")
+    dt = _dtype_code(vals)
+    if out is None:
+        out = torch.empty(n_groups, dtype=vals.dtype)
+    st = _lib.repro_groupby_sum_host(keys.data_ptr() if keys.numel() else None,
+                                     vals.data_ptr() if vals.numel() else None, keys.numel(), n_groups, fold,
+                                     dt, out.data_ptr())
+    _check(st, "repro_groupby_sum_host")
+    return out
+
+
+def baseline_atomic_sum(keys, vals, n_groups: int, variant: int = 0, accumulate_f64: bool = False, out=None,
+                        stream=None):
+    """Non-reproducible atomicAdd GroupBy on the same GPU (stream-ordered)."""
+    torch = _torch()
+    dt = _dtype_code(vals)
+    odt = torch.float64 if (dt == F64 or accumulate_f64) else torch.float32
+    if out is None:
+        out = torch.empty(n_groups, dtype=odt, device=vals.device)
+    st = _lib.repro_baseline_atomic_sum(_dev(keys, "keys", torch.int32), _dev(vals, "vals"), keys.numel(), n_groups,
+                                        dt, variant, 1 if accumulate_f64 else 0, _dev(out, "out", odt),
+                                        _stream_ptr(stream))
+    _check(st, "repro_baseline_atomic_sum")
+    return out
+
+
+def last_launch_count() -> int:
+    return _lib.repro_last_launch_count()
+
+
+def last_path() -> int:
+    return _lib.repro_last_path()
+
+
+def onchip_max_groups(fold: int, dtype: int) -> int:
+    return _lib.repro_onchip_max_groups(fold, dtype)
+
+
+def set_path_override(path: int):
+    _lib.repro_set_path_override(path)
+
+
+def set_kernel_variant(variant: int):
+    """0 auto, 1 per-row shared atomics, 2 tile-sorted runs (bits never change)."""
+    _lib.repro_set_kernel_variant(variant)
+
+
+def timing_enable(on: bool = True):
+    """Bracket every kernel this thread enqueues with CUDA events (bench aid)."""
+    _lib.repro_timing_enable(1 if on else 0)
+
+
+def timing_collect() -> dict:
+    """{kernel name: (launches, total device ms)} since the last collect."""
+    names = (ctypes.c_char_p * 32)()
+    counts = (_i32 * 32)()
+    ms = (ctypes.c_double * 32)()
+    k = _lib.repro_timing_collect(names, counts, ms, 32)
+    return {names[i].decode(): (counts[i], ms[i]) for i in range(k)}
+
+
+def release_cache():
+    _lib.repro_release_cache()
+
+
+class Accumulator:
+    """n_groups device-resident repro<ScalarT, fold> states (repro_acc_*)."""
+
+    def __init__(self, n_groups: int, fold: int = 3, dtype: int = F64):
+        h = _vp()
+        _check(_lib.repro_acc_create(ctypes.byref(h), n_groups, fold, dtype), "repro_acc_create")
+        self._h = h
+        self.n_groups, self.fold, self.dtype = n_groups, fold, dtype
+
+    @property
+    def _torch_dtype(self):
+        torch = _torch()
+        return torch.float64 if self.dtype == F64 else torch.float32
+
+    def deposit(self, keys, vals):
+        torch = _torch()
+        if _dtype_code(vals) != self.dtype:
+            raise TypeError("value dtype does not match the accumulator")
+        _check(_lib.repro_acc_deposit(self._h, _dev(keys, "keys", torch.int32), _dev(vals, "vals"), keys.numel()),
+               "repro_acc_deposit")
+        return self
+
+    def merge(self, other: "Accumulator"):
+        _check(_lib.repro_acc_merge(self._h, other._h), "repro_acc_merge")
+        return self
+
+    def finalize(self, out=None):
+        torch = _torch()
+        if out is None:
+            out = torch.empty(self.n_groups, dtype=self._torch_dtype, device="cuda")
+        _check(_lib.repro_acc_finalize(self._h, _dev(out, "out", self._torch_dtype)), "repro_acc_finalize")
+        return out
+
+    def export(self, state=None):
+        torch = _torch()
+        if state is None:
+            state = torch.empty(self.n_groups * 2 * self.fold, dtype=self._torch_dtype, device="cuda")
+        _check(_lib.repro_acc_export(self._h, _dev(state, "state", self._torch_dtype)), "repro_acc_export")
+        return state
+
+    def import_(self, state):
+        _check(_lib.repro_acc_import(self._h, _dev(state, "state", self._torch_dtype)), "repro_acc_import")
+        return self
+
+    def reset(self):
+        _check(_lib.repro_acc_reset(self._h), "repro_acc_reset")
+        return self
+
+    def top_levels(self, out=None):
+        torch = _torch()
+        if out is None:
+            out = torch.empty(self.n_groups, dtype=torch.int32, device="cuda")
+        _check(_lib.repro_acc_top_levels(self._h, _dev(out, "k", torch.int32)), "repro_acc_top_levels")
+        return out
+
+    def window_export(self, k_global, limbs=None):
+        torch = _torch()
+        if limbs is None:
+            limbs = torch.empty(self.n_groups * self.fold * 2, dtype=torch.int64, device="cuda")
+        _check(_lib.repro_acc_window_export(self._h, _dev(k_global, "k_global", torch.int32),
+                                            _dev(limbs, "limbs", torch.int64)), "repro_acc_window_export")
+        return limbs
+
+    def window_import(self, k_global, limbs, g0: int = 0, count: int | None = None):
+        torch = _torch()
+        count = self.n_groups - g0 if count is None else count
+        _check(_lib.repro_acc_window_import_range(self._h, g0, count, _dev(k_global, "k_global", torch.int32),
+                                                  _dev(limbs, "limbs", torch.int64)),
+               "repro_acc_window_import_range")
+        return self
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.repro_acc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

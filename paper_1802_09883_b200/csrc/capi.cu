@@ -1,0 +1,595 @@
+// capi.cu -- host orchestration behind the C-ABI of include/repro_groupby.h:
+// argument validation, path choice (on-chip tables vs radix partitioning),
+// workspace layout, launches, device status word.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+#include "repro_groupby.h"
+
+namespace repro {
+
+const DeviceProps &device_props() {
+    static DeviceProps props[64];
+    static bool have[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!have[dev]) {
+        DeviceProps p{};
+        p.device = dev;
+        cudaDeviceGetAttribute(&p.sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaDeviceGetAttribute(&p.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        if (p.sms <= 0) p.sms = 148;
+        if (p.smem_optin <= 0) p.smem_optin = 227 * 1024;
+        props[dev] = p;
+        have[dev] = true;
+    }
+    return props[dev];
+}
+
+}  // namespace repro
+
+using namespace repro;
+
+namespace {
+
+thread_local int32_t t_launches = 0;
+thread_local int32_t t_path = -1;
+int32_t g_path_override = -1;
+
+// ---- per-kernel event timing (repro_timing_enable / _collect) -------------
+struct TimingRec {
+    const char *name;
+    cudaEvent_t a, b;
+};
+thread_local bool t_timing = false;
+thread_local std::vector<TimingRec> t_recs;
+thread_local std::vector<cudaEvent_t> t_pool;
+
+cudaEvent_t pool_event() {
+    if (!t_pool.empty()) {
+        cudaEvent_t e = t_pool.back();
+        t_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Run one launcher; when timing is on, bracket it with events on `st`.
+template <class Fn>
+int timed(const char *name, cudaStream_t st, Fn &&fn) {
+    if (!t_timing) return fn();
+    cudaEvent_t a = pool_event(), b = pool_event();
+    cudaEventRecord(a, st);
+    const int rc = fn();
+    cudaEventRecord(b, st);
+    t_recs.push_back({name, a, b});
+    return rc;
+}
+
+constexpr size_t ALIGN = 256;
+inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
+
+int status_from_flags(uint32_t f) {
+    if (f & FLAG_EINVAL) return REPRO_EINVAL;
+    if (f & FLAG_EKEY) return REPRO_EKEY;
+    if (f & FLAG_EDOM) return REPRO_EDOM;
+    if (f & FLAG_ERANGE) return REPRO_ERANGE;
+    return REPRO_OK;
+}
+
+int map_launch(int rc) { return rc == 0 ? REPRO_OK : (rc == -1 ? REPRO_EINVAL : REPRO_ECUDA); }
+
+bool valid_shape(int32_t G, int32_t K, int32_t dt) {
+    return G >= 1 && K >= 1 && K <= 4 && (dt == REPRO_F32 || dt == REPRO_F64);
+}
+
+// 0 = on-chip, 1 = partitioned, -1 = not supported
+int choose_path(int32_t G, int32_t K, int32_t dt) {
+    const int onchip = onchip_max_groups(K, dt);
+    if (g_path_override == 0) return G <= onchip ? 0 : -1;
+    if (g_path_override == 1) return G <= partition_max_groups(K, dt) ? 1 : -1;
+    if (G <= onchip) return 0;
+    return G <= partition_max_groups(K, dt) ? 1 : -1;
+}
+
+// on-chip workspace: [flags | kglob int32[G] | slots u64[G][NS][2]]
+struct OnchipWs {
+    uint32_t *flags;
+    int32_t *kglob;
+    unsigned long long *slots;
+    size_t zero_bytes;  // bytes from flags to the end of slots (one memset)
+};
+
+size_t onchip_ws_bytes(int32_t G, int32_t K, int32_t dt) {
+    return ALIGN + align_up(sizeof(int32_t) * (size_t)G) +
+           align_up(sizeof(unsigned long long) * 2 * (size_t)G * slot_count(dt, K));
+}
+
+OnchipWs carve_onchip(void *ws, int32_t G, int32_t K, int32_t dt) {
+    OnchipWs w;
+    char *p = (char *)ws;
+    w.flags = (uint32_t *)p;
+    w.kglob = (int32_t *)(p + ALIGN);
+    w.slots = (unsigned long long *)(p + ALIGN + align_up(sizeof(int32_t) * (size_t)G));
+    w.zero_bytes = onchip_ws_bytes(G, K, dt);
+    return w;
+}
+
+size_t ws_bytes_for(int path, int64_t n, int32_t G, int32_t K, int32_t dt) {
+    if (path == 0) return onchip_ws_bytes(G, K, dt);
+    return ALIGN + partition_workspace_bytes(n, G, K, dt);
+}
+
+// Library-internal workspace cache for the blocking entry points.
+struct Cache {
+    std::mutex mu;
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    int device = -1;
+} g_cache;
+
+void *cache_get(size_t bytes) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_cache.ptr && (g_cache.bytes < bytes || g_cache.device != dev)) {
+        cudaFree(g_cache.ptr);
+        g_cache.ptr = nullptr;
+        g_cache.bytes = 0;
+    }
+    if (!g_cache.ptr) {
+        size_t want = std::max(bytes, (size_t)1 << 20);
+        if (cudaMalloc(&g_cache.ptr, want) != cudaSuccess) {
+            cudaGetLastError();
+            g_cache.ptr = nullptr;
+            return nullptr;
+        }
+        g_cache.bytes = want;
+        g_cache.device = dev;
+    }
+    return g_cache.ptr;
+}
+
+// Enqueue the whole GroupBy (deposit into a fresh slot table / partitions,
+// then fold + Eq. 1 into out, or merge into an accumulator).
+int enqueue_groupby(const int32_t *keys, const void *vals, int64_t n, int32_t G, int32_t K, int32_t dt,
+                    void *out, int merge, int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *ws,
+                    size_t ws_bytes, cudaStream_t st, uint32_t **flags_out) {
+    const int path = choose_path(G, K, dt);
+    t_path = path;
+    if (path < 0) return REPRO_EINVAL;
+    if (ws_bytes < ws_bytes_for(path, n, G, K, dt)) return REPRO_ENOMEM;
+    if (path == 0) {
+        OnchipWs w = carve_onchip(ws, G, K, dt);
+        *flags_out = w.flags;
+        if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
+        int rc = timed("onchip_accumulate", st, [&] {
+            return launch_onchip_any(dt, K, keys, vals, n, G, w.kglob, w.slots, w.flags, st, &t_launches);
+        });
+        if (rc) return map_launch(rc);
+        rc = timed("fold", st, [&] {
+            return launch_fold(dt, K, G, w.kglob, w.slots, merge, acc_k, acc_C, acc_D, out, w.flags, st,
+                               &t_launches);
+        });
+        return map_launch(rc);
+    }
+    uint32_t *flags = (uint32_t *)ws;
+    *flags_out = flags;
+    if (cudaMemsetAsync(flags, 0, ALIGN, st) != cudaSuccess) return REPRO_ECUDA;
+    int rc = launch_partitioned(dt, K, keys, vals, n, G, (char *)ws + ALIGN, ws_bytes - ALIGN, merge, acc_k,
+                                acc_C, acc_D, out, flags, st, &t_launches);
+    return map_launch(rc);
+}
+
+int finish_blocking(uint32_t *d_flags, cudaStream_t st) {
+    uint32_t f = 0;
+    if (cudaMemcpyAsync(&f, d_flags, sizeof f, cudaMemcpyDeviceToHost, st) != cudaSuccess) return REPRO_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return REPRO_ECUDA;
+    return status_from_flags(f);
+}
+
+}  // namespace
+
+struct repro_acc {
+    int32_t G, K, dt;
+    int32_t *k;
+    int64_t *C;
+    int64_t *D;
+};
+
+extern "C" {
+
+const char *repro_strerror(int status) {
+    switch (status) {
+        case REPRO_OK: return "ok";
+        case REPRO_EINVAL: return "invalid argument";
+        case REPRO_EKEY: return "key outside [0, n_groups)";
+        case REPRO_EDOM: return "NaN or infinite value";
+        case REPRO_ERANGE: return "value or carry count outside the representable range";
+        case REPRO_ECUDA: return "CUDA error";
+        case REPRO_ENOMEM: return "out of memory / workspace too small";
+        default: return "unknown status";
+    }
+}
+
+const char *repro_version(void) { return "repro_b200 0.1 (sm_100a)"; }
+
+int32_t repro_last_launch_count(void) { return t_launches; }
+int32_t repro_last_path(void) { return t_path; }
+int32_t repro_onchip_max_groups(int32_t fold, int32_t dtype) {
+    if (fold < 1 || fold > 4 || (dtype != 0 && dtype != 1)) return 0;
+    return onchip_max_groups(fold, dtype);
+}
+void repro_set_kernel_variant(int32_t variant) { set_onchip_variant(variant); }
+
+void repro_timing_enable(int32_t on) { t_timing = on != 0; }
+
+int32_t repro_timing_collect(const char **names, int32_t *counts, double *total_ms, int32_t max) {
+    std::vector<const char *> nm;
+    std::vector<int32_t> cnt;
+    std::vector<double> ms;
+    for (auto &r : t_recs) {
+        cudaEventSynchronize(r.b);
+        float e = 0.f;
+        cudaEventElapsedTime(&e, r.a, r.b);
+        size_t i = 0;
+        while (i < nm.size() && std::string(nm[i]) != r.name) ++i;
+        if (i == nm.size()) {
+            nm.push_back(r.name);
+            cnt.push_back(0);
+            ms.push_back(0.0);
+        }
+        cnt[i] += 1;
+        ms[i] += e;
+        t_pool.push_back(r.a);
+        t_pool.push_back(r.b);
+    }
+    t_recs.clear();
+    const int32_t k = (int32_t)std::min<size_t>(nm.size(), (size_t)std::max(max, 0));
+    for (int32_t i = 0; i < k; ++i) {
+        if (names) names[i] = nm[i];
+        if (counts) counts[i] = cnt[i];
+        if (total_ms) total_ms[i] = ms[i];
+    }
+    return k;
+}
+
+void repro_set_path_override(int32_t path) { g_path_override = (path == 0 || path == 1) ? path : -1; }
+
+size_t repro_groupby_workspace_bytes(int64_t n, int32_t n_groups, int32_t fold, int32_t dtype) {
+    if (n < 0 || !valid_shape(n_groups, fold, dtype)) return 0;
+    const int path = choose_path(n_groups, fold, dtype);
+    if (path < 0) return 0;
+    return ws_bytes_for(path, n, n_groups, fold, dtype);
+}
+
+int repro_groupby_sum_async(const int32_t *keys, const void *vals, int64_t n, int32_t n_groups, int32_t fold,
+                            int32_t dtype, void *out, void *workspace, size_t ws_bytes, void *stream,
+                            int32_t *d_status) {
+    t_launches = 0;
+    if (n < 0 || !valid_shape(n_groups, fold, dtype) || !out || !workspace || !d_status) return REPRO_EINVAL;
+    if (n > 0 && (!keys || !vals)) return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *flags = nullptr;
+    int rc = enqueue_groupby(keys, vals, n, n_groups, fold, dtype, out, 0, nullptr, nullptr, nullptr, workspace,
+                             ws_bytes, st, &flags);
+    if (rc != REPRO_OK) return rc;
+    return map_launch(timed("status", st, [&] { return launch_status(flags, d_status, st, &t_launches); }));
+}
+
+int repro_groupby_sum(const int32_t *keys, const void *vals, int64_t n, int32_t n_groups, int32_t fold,
+                      int32_t dtype, void *out) {
+    t_launches = 0;
+    if (n < 0 || !valid_shape(n_groups, fold, dtype) || !out) return REPRO_EINVAL;
+    if (n > 0 && (!keys || !vals)) return REPRO_EINVAL;
+    const size_t need = repro_groupby_workspace_bytes(n, n_groups, fold, dtype);
+    if (need == 0) return REPRO_EINVAL;
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    void *ws = cache_get(need);
+    if (!ws) return REPRO_ENOMEM;
+    uint32_t *flags = nullptr;
+    int rc = enqueue_groupby(keys, vals, n, n_groups, fold, dtype, out, 0, nullptr, nullptr, nullptr, ws, need,
+                             0, &flags);
+    if (rc != REPRO_OK) {
+        cudaStreamSynchronize(0);
+        return rc;
+    }
+    return finish_blocking(flags, 0);
+}
+
+void repro_release_cache(void) {
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    if (g_cache.ptr) cudaFree(g_cache.ptr);
+    g_cache.ptr = nullptr;
+    g_cache.bytes = 0;
+}
+
+// Host-array variant: rows are streamed to the device in chunks on a copy
+// stream while the on-chip kernel deposits the previous chunk into the same
+// absolute-level slot table (exact whatever the chunking), then one fold.
+int repro_groupby_sum_host(const int32_t *keys_host, const void *vals_host, int64_t n, int32_t n_groups,
+                           int32_t fold, int32_t dtype, void *out_host) {
+    t_launches = 0;
+    if (n < 0 || !valid_shape(n_groups, fold, dtype) || !out_host) return REPRO_EINVAL;
+    if (n > 0 && (!keys_host || !vals_host)) return REPRO_EINVAL;
+    const size_t vsz = dtype == REPRO_F64 ? 8 : 4;
+    const int path = choose_path(n_groups, fold, dtype);
+    if (path < 0) return REPRO_EINVAL;
+    int status = REPRO_OK;
+    cudaStream_t cs = nullptr, ks = nullptr;
+    cudaEvent_t copied[2] = {}, consumed[2] = {};
+    void *dbuf = nullptr, *dout = nullptr, *ws = nullptr;
+    void *pin[2] = {};
+    bool pinned_input = false;
+    {
+        cudaPointerAttributes a{};
+        if (n > 0 && cudaPointerGetAttributes(&a, keys_host) == cudaSuccess && a.type == cudaMemoryTypeHost) {
+            cudaPointerAttributes b{};
+            pinned_input = cudaPointerGetAttributes(&b, vals_host) == cudaSuccess && b.type == cudaMemoryTypeHost;
+        }
+        cudaGetLastError();
+    }
+    const int64_t CH = path == 0 ? ((int64_t)1 << 23) : std::max<int64_t>(n, 1);
+    const int nb = path == 0 ? 2 : 1;
+    const size_t chunk_bytes = (size_t)std::min<int64_t>(CH, std::max<int64_t>(n, 1)) * (4 + vsz);
+#define CK(x)                                    \
+    do {                                         \
+        if ((x) != cudaSuccess) {                \
+            status = REPRO_ECUDA;                \
+            goto done;                           \
+        }                                        \
+    } while (0)
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&consumed[b], cudaEventDisableTiming));
+    }
+    CK(cudaMalloc(&dbuf, chunk_bytes * nb + ALIGN));
+    CK(cudaMalloc(&dout, vsz * (size_t)n_groups));
+    {
+        const size_t need = ws_bytes_for(path, n, n_groups, fold, dtype);
+        CK(cudaMalloc(&ws, need));
+        if (!pinned_input)
+            for (int b = 0; b < nb; ++b) CK(cudaMallocHost(&pin[b], chunk_bytes));
+        if (path == 0) {
+            OnchipWs w = carve_onchip(ws, n_groups, fold, dtype);
+            CK(cudaMemsetAsync(ws, 0, w.zero_bytes, ks));
+            int c = 0;
+            for (int64_t r0 = 0; r0 < n; r0 += CH, ++c) {
+                const int b = c % nb;
+                const int64_t rows = std::min<int64_t>(CH, n - r0);
+                char *dk = (char *)dbuf + (size_t)b * chunk_bytes;
+                char *dv = dk + align_up((size_t)rows * 4);
+                if (c >= nb) CK(cudaEventSynchronize(consumed[b]));  // host staging + device buffer free
+                const char *hk = (const char *)keys_host + (size_t)r0 * 4;
+                const char *hv = (const char *)vals_host + (size_t)r0 * vsz;
+                if (!pinned_input) {
+                    memcpy(pin[b], hk, (size_t)rows * 4);
+                    memcpy((char *)pin[b] + align_up((size_t)rows * 4), hv, (size_t)rows * vsz);
+                    hk = (const char *)pin[b];
+                    hv = (const char *)pin[b] + align_up((size_t)rows * 4);
+                }
+                CK(cudaMemcpyAsync(dk, hk, (size_t)rows * 4, cudaMemcpyHostToDevice, cs));
+                CK(cudaMemcpyAsync(dv, hv, (size_t)rows * vsz, cudaMemcpyHostToDevice, cs));
+                CK(cudaEventRecord(copied[b], cs));
+                CK(cudaStreamWaitEvent(ks, copied[b], 0));
+                int rc = timed("onchip_accumulate", ks, [&] {
+                    return launch_onchip_any(dtype, fold, (const int32_t *)dk, dv, rows, n_groups, w.kglob,
+                                             w.slots, w.flags, ks, &t_launches);
+                });
+                if (rc) { status = map_launch(rc); goto done; }
+                CK(cudaEventRecord(consumed[b], ks));
+            }
+            int rc = timed("fold", ks, [&] {
+                return launch_fold(dtype, fold, n_groups, w.kglob, w.slots, 0, nullptr, nullptr, nullptr, dout,
+                                   w.flags, ks, &t_launches);
+            });
+            if (rc) { status = map_launch(rc); goto done; }
+            CK(cudaMemcpyAsync(out_host, dout, vsz * (size_t)n_groups, cudaMemcpyDeviceToHost, ks));
+            status = finish_blocking(w.flags, ks);
+        } else {
+            char *dk = (char *)dbuf;
+            char *dv = dk + align_up((size_t)n * 4);
+            CK(cudaMemcpyAsync(dk, keys_host, (size_t)n * 4, cudaMemcpyHostToDevice, ks));
+            CK(cudaMemcpyAsync(dv, vals_host, (size_t)n * vsz, cudaMemcpyHostToDevice, ks));
+            uint32_t *flags = nullptr;
+            int rc = enqueue_groupby((const int32_t *)dk, dv, n, n_groups, fold, dtype, dout, 0, nullptr, nullptr,
+                                     nullptr, ws, need, ks, &flags);
+            if (rc != REPRO_OK) { status = rc; goto done; }
+            CK(cudaMemcpyAsync(out_host, dout, vsz * (size_t)n_groups, cudaMemcpyDeviceToHost, ks));
+            status = finish_blocking(flags, ks);
+        }
+    }
+done:
+#undef CK
+    if (ks) cudaStreamSynchronize(ks);
+    if (cs) cudaStreamSynchronize(cs);
+    for (int b = 0; b < 2; ++b) {
+        if (pin[b]) cudaFreeHost(pin[b]);
+        if (copied[b]) cudaEventDestroy(copied[b]);
+        if (consumed[b]) cudaEventDestroy(consumed[b]);
+    }
+    if (dbuf) cudaFree(dbuf);
+    if (dout) cudaFree(dout);
+    if (ws) cudaFree(ws);
+    if (cs) cudaStreamDestroy(cs);
+    if (ks) cudaStreamDestroy(ks);
+    return status;
+}
+
+// ---------------------------------------------------------------------------
+// accumulator handles
+// ---------------------------------------------------------------------------
+
+int repro_acc_create(repro_acc **acc, int32_t n_groups, int32_t fold, int32_t dtype) {
+    t_launches = 0;
+    if (!acc || !valid_shape(n_groups, fold, dtype)) return REPRO_EINVAL;
+    repro_acc *a = (repro_acc *)calloc(1, sizeof(repro_acc));
+    if (!a) return REPRO_ENOMEM;
+    a->G = n_groups;
+    a->K = fold;
+    a->dt = dtype;
+    if (cudaMalloc(&a->k, sizeof(int32_t) * (size_t)n_groups) != cudaSuccess ||
+        cudaMalloc(&a->C, sizeof(int64_t) * (size_t)n_groups * fold) != cudaSuccess ||
+        cudaMalloc(&a->D, sizeof(int64_t) * (size_t)n_groups * fold) != cudaSuccess) {
+        cudaGetLastError();
+        repro_acc_destroy(a);
+        return REPRO_ENOMEM;
+    }
+    if (launch_reset(fold, n_groups, a->k, a->C, a->D, 0, &t_launches) != 0 || cudaStreamSynchronize(0) != cudaSuccess) {
+        repro_acc_destroy(a);
+        return REPRO_ECUDA;
+    }
+    *acc = a;
+    return REPRO_OK;
+}
+
+void repro_acc_destroy(repro_acc *acc) {
+    if (!acc) return;
+    if (acc->k) cudaFree(acc->k);
+    if (acc->C) cudaFree(acc->C);
+    if (acc->D) cudaFree(acc->D);
+    free(acc);
+}
+
+int32_t repro_acc_n_groups(const repro_acc *acc) { return acc ? acc->G : 0; }
+int32_t repro_acc_fold(const repro_acc *acc) { return acc ? acc->K : 0; }
+int32_t repro_acc_dtype(const repro_acc *acc) { return acc ? acc->dt : -1; }
+
+int repro_acc_reset(repro_acc *acc) {
+    t_launches = 0;
+    if (!acc) return REPRO_EINVAL;
+    if (launch_reset(acc->K, acc->G, acc->k, acc->C, acc->D, 0, &t_launches) != 0) return REPRO_ECUDA;
+    return cudaStreamSynchronize(0) == cudaSuccess ? REPRO_OK : REPRO_ECUDA;
+}
+
+int repro_acc_deposit(repro_acc *acc, const int32_t *keys, const void *vals, int64_t n) {
+    t_launches = 0;
+    if (!acc || n < 0 || (n > 0 && (!keys || !vals))) return REPRO_EINVAL;
+    if (n == 0) return REPRO_OK;
+    const size_t need = repro_groupby_workspace_bytes(n, acc->G, acc->K, acc->dt);
+    if (need == 0) return REPRO_EINVAL;
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    void *ws = cache_get(need);
+    if (!ws) return REPRO_ENOMEM;
+    uint32_t *flags = nullptr;
+    int rc = enqueue_groupby(keys, vals, n, acc->G, acc->K, acc->dt, nullptr, 1, acc->k, acc->C, acc->D, ws, need, 0,
+                             &flags);
+    if (rc != REPRO_OK) {
+        cudaStreamSynchronize(0);
+        return rc;
+    }
+    return finish_blocking(flags, 0);
+}
+
+static int run_small(int launch_rc, uint32_t *flags) {
+    if (launch_rc) {
+        cudaStreamSynchronize(0);
+        return map_launch(launch_rc);
+    }
+    return finish_blocking(flags, 0);
+}
+
+static uint32_t *small_flags() {
+    void *ws = cache_get(ALIGN);
+    if (!ws) return nullptr;
+    if (cudaMemsetAsync(ws, 0, sizeof(uint32_t), 0) != cudaSuccess) return nullptr;
+    return (uint32_t *)ws;
+}
+
+int repro_acc_merge(repro_acc *dst, const repro_acc *src) {
+    t_launches = 0;
+    if (!dst || !src || dst->G != src->G || dst->K != src->K || dst->dt != src->dt) return REPRO_EINVAL;
+    if (dst == src) return REPRO_EINVAL;
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    uint32_t *f = small_flags();
+    if (!f) return REPRO_ENOMEM;
+    return run_small(launch_merge_state(dst->dt, dst->K, dst->G, dst->k, dst->C, dst->D, src->k, src->C, src->D, f, 0,
+                                        &t_launches),
+                     f);
+}
+
+int repro_acc_finalize(const repro_acc *acc, void *out) {
+    t_launches = 0;
+    if (!acc || !out) return REPRO_EINVAL;
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    uint32_t *f = small_flags();
+    if (!f) return REPRO_ENOMEM;
+    return run_small(launch_finalize(acc->dt, acc->K, acc->G, acc->k, acc->C, acc->D, out, f, 0, &t_launches), f);
+}
+
+int repro_acc_export(const repro_acc *acc, void *state) {
+    t_launches = 0;
+    if (!acc || !state) return REPRO_EINVAL;
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    uint32_t *f = small_flags();
+    if (!f) return REPRO_ENOMEM;
+    return run_small(launch_export(acc->dt, acc->K, acc->G, acc->k, acc->C, acc->D, state, f, 0, &t_launches), f);
+}
+
+int repro_acc_import(repro_acc *acc, const void *state) {
+    t_launches = 0;
+    if (!acc || !state) return REPRO_EINVAL;
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    uint32_t *f = small_flags();
+    if (!f) return REPRO_ENOMEM;
+    return run_small(launch_import(acc->dt, acc->K, acc->G, state, acc->k, acc->C, acc->D, f, 0, &t_launches), f);
+}
+
+int repro_acc_top_levels(const repro_acc *acc, int32_t *k_out) {
+    t_launches = 0;
+    if (!acc || !k_out) return REPRO_EINVAL;
+    if (cudaMemcpyAsync(k_out, acc->k, sizeof(int32_t) * (size_t)acc->G, cudaMemcpyDeviceToDevice, 0) != cudaSuccess)
+        return REPRO_ECUDA;
+    return cudaStreamSynchronize(0) == cudaSuccess ? REPRO_OK : REPRO_ECUDA;
+}
+
+int repro_acc_window_export(const repro_acc *acc, const int32_t *k_global, int64_t *limbs_out) {
+    t_launches = 0;
+    if (!acc || !k_global || !limbs_out) return REPRO_EINVAL;
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    uint32_t *f = small_flags();
+    if (!f) return REPRO_ENOMEM;
+    return run_small(launch_window_export(acc->dt, acc->K, acc->G, acc->k, acc->C, acc->D, k_global, limbs_out, f, 0,
+                                          &t_launches),
+                     f);
+}
+
+int repro_acc_window_import_range(repro_acc *acc, int32_t g0, int32_t count, const int32_t *k_global,
+                                  const int64_t *limbs) {
+    t_launches = 0;
+    if (!acc || !k_global || !limbs || g0 < 0 || count < 0 || (int64_t)g0 + count > acc->G) return REPRO_EINVAL;
+    if (count == 0) return REPRO_OK;
+    int rc = launch_window_import(acc->dt, acc->K, count, k_global, limbs, acc->k + g0, acc->C + (size_t)g0 * acc->K,
+                                  acc->D + (size_t)g0 * acc->K, nullptr, 0, &t_launches);
+    if (rc) return map_launch(rc);
+    return cudaStreamSynchronize(0) == cudaSuccess ? REPRO_OK : REPRO_ECUDA;
+}
+
+int repro_acc_window_import(repro_acc *acc, const int32_t *k_global, const int64_t *limbs) {
+    if (!acc) return REPRO_EINVAL;
+    return repro_acc_window_import_range(acc, 0, acc->G, k_global, limbs);
+}
+
+int repro_baseline_atomic_sum(const int32_t *keys, const void *vals, int64_t n, int32_t n_groups, int32_t dtype,
+                              int32_t variant, int32_t accumulate_f64, void *out, void *stream) {
+    t_launches = 0;
+    if (n < 0 || n_groups < 1 || (dtype != 0 && dtype != 1) || !out || (n > 0 && (!keys || !vals)))
+        return REPRO_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    return map_launch(timed(variant == 0 ? "baseline_atomic_global" : "baseline_atomic_smem", st, [&] {
+        return launch_baseline(dtype, variant, accumulate_f64, keys, vals, n, n_groups, out, st, &t_launches);
+    }));
+}
+
+}  // extern "C"

@@ -1,0 +1,74 @@
+// internal.h -- host-side declarations shared by the .cu files of the library
+// (not part of the C-ABI; see include/repro_groupby.h).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace repro {
+
+struct DeviceProps {
+    int device;
+    int sms;
+    int smem_optin;  // max dynamic shared memory per block (opt-in)
+};
+const DeviceProps &device_props();
+
+// Number of absolute lattice slots of a group's slot table: levels
+// -(K-1) .. KMAX, slot = level + K - 1.
+inline int slot_count(int DT, int K) { return (DT == 1 ? 25 : 7) + K; }
+
+// ---- launchers (return 0 on success, -1 unsupported shape, -2 CUDA error) --
+int onchip_max_groups(int K, int DT);
+void set_onchip_variant(int v);
+int sorted_max_groups(int K, int DT);
+int atomic_max_groups(int K, int DT);
+int launch_sorted_any(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
+                      int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
+                      int *launches);
+int launch_atomic_any(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
+                      int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
+                      int *launches);
+int launch_onchip_any(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
+                      int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
+                      int *launches);
+
+// slots (+ global tops) -> canonical state; optionally merged with the
+// existing state (acc_*), optionally finalised into out.  `merge` != 0 reads
+// acc_k/acc_C/acc_D as the previous state.
+int launch_fold(int DT, int K, int32_t G, const int32_t *kglob, const unsigned long long *slots,
+                int merge, int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *out,
+                uint32_t *status, cudaStream_t st, int *launches);
+
+// canonical state -> Eq. 1 read-out
+int launch_finalize(int DT, int K, int32_t G, const int32_t *k, const int64_t *C, const int64_t *D,
+                    void *out, uint32_t *status, cudaStream_t st, int *launches);
+int launch_export(int DT, int K, int32_t G, const int32_t *k, const int64_t *C, const int64_t *D,
+                  void *state, uint32_t *status, cudaStream_t st, int *launches);
+int launch_import(int DT, int K, int32_t G, const void *state, int32_t *k, int64_t *C, int64_t *D,
+                  uint32_t *status, cudaStream_t st, int *launches);
+int launch_merge_state(int DT, int K, int32_t G, int32_t *dk, int64_t *dC, int64_t *dD,
+                       const int32_t *sk, const int64_t *sC, const int64_t *sD, uint32_t *status,
+                       cudaStream_t st, int *launches);
+int launch_reset(int K, int32_t G, int32_t *k, int64_t *C, int64_t *D, cudaStream_t st, int *launches);
+int launch_window_export(int DT, int K, int32_t G, const int32_t *k, const int64_t *C,
+                         const int64_t *D, const int32_t *kg, int64_t *limbs, uint32_t *status,
+                         cudaStream_t st, int *launches);
+int launch_window_import(int DT, int K, int32_t count, const int32_t *kg, const int64_t *limbs,
+                         int32_t *k, int64_t *C, int64_t *D, uint32_t *status, cudaStream_t st,
+                         int *launches);
+int launch_status(const uint32_t *flags, int32_t *d_status, cudaStream_t st, int *launches);
+
+// ---- partitioned (high-cardinality) path --------------------------------
+int partition_max_groups(int K, int DT);
+size_t partition_workspace_bytes(int64_t n, int32_t G, int K, int DT);
+int launch_partitioned(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
+                       void *ws, size_t ws_bytes, int merge, int32_t *acc_k, int64_t *acc_C,
+                       int64_t *acc_D, void *out, uint32_t *status, cudaStream_t st, int *launches);
+
+// ---- non-reproducible baseline --------------------------------------------
+int launch_baseline(int DT, int variant, int acc64, const int32_t *keys, const void *vals,
+                    int64_t n, int32_t G, void *out, cudaStream_t st, int *launches);
+
+}  // namespace repro
