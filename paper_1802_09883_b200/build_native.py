@@ -16,7 +16,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
-LIB = os.path.join(LIBDIR, "librepro_b200.so")
+LIB = os.environ.get("REPRO_B200_LIB") or os.path.join(LIBDIR, "librepro_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
@@ -36,22 +36,24 @@ def stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Compile the library (to `out`, default LIB) with optional -D defines."""
+    target = out or LIB
+    if not force and out is None and not stale():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, "-shared", "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *sources(), "-o", LIB + ".tmp"]
+    os.makedirs(os.path.dirname(target), exist_ok=True)
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-shared", "-I", os.path.join(ROOT, "include"),
+           "-I", CSRC, *sources(), "-o", target + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     with open(os.path.join(LIBDIR, "build.log"), "w") as fh:
         fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)
         raise RuntimeError("nvcc failed building librepro_b200.so")
-    os.replace(LIB + ".tmp", LIB)
+    os.replace(target + ".tmp", target)
     if verbose:
         print(res.stderr)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":
