@@ -63,6 +63,29 @@ cudaEvent_t pool_event() {
     return e;
 }
 
+thread_local std::vector<cudaEvent_t> t_open;
+
+}  // namespace
+
+namespace repro {
+int trace_begin(cudaStream_t st) {
+    if (!t_timing) return -1;
+    cudaEvent_t a = pool_event();
+    cudaEventRecord(a, st);
+    t_open.push_back(a);
+    return (int)t_open.size() - 1;
+}
+void trace_end(int token, const char *name, cudaStream_t st) {
+    if (token < 0 || token >= (int)t_open.size()) return;
+    cudaEvent_t b = pool_event();
+    cudaEventRecord(b, st);
+    t_recs.push_back({name, t_open[token], b});
+    if (token == (int)t_open.size() - 1) t_open.pop_back();
+}
+}  // namespace repro
+
+namespace {
+
 // Run one launcher; when timing is on, bracket it with events on `st`.
 template <class Fn>
 int timed(const char *name, cudaStream_t st, Fn &&fn) {

@@ -60,6 +60,12 @@ int launch_window_import(int DT, int K, int32_t count, const int32_t *kg, const 
                          int *launches);
 int launch_status(const uint32_t *flags, int32_t *d_status, cudaStream_t st, int *launches);
 
+// ---- per-kernel event timing (repro_timing_enable) ------------------------
+// trace_begin returns a token (or -1 when timing is off); trace_end records
+// the kernel named `name` between the two events on `st`.
+int trace_begin(cudaStream_t st);
+void trace_end(int token, const char *name, cudaStream_t st);
+
 // ---- partitioned (high-cardinality) path --------------------------------
 int partition_max_groups(int K, int DT);
 size_t partition_workspace_bytes(int64_t n, int32_t G, int K, int DT);

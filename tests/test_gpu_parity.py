@@ -343,3 +343,89 @@ def test_atomic_baseline_close_to_repro(R):
     for variant in (0, 1):
         b = R.baseline_atomic_sum(dev(keys), dev(vals), 1024, variant=variant).cpu().numpy()
         np.testing.assert_allclose(b, rep, rtol=1e-9, atol=1e-6)
+
+
+# ------------------------------------------------- partitioned path (row a5)
+
+@pytest.fixture
+def partitioned(R):
+    R.set_path_override(1)
+    yield
+    R.set_path_override(-1)
+
+
+PART_CASES = [
+    (np.float64, 3, 1, 30001, 20),
+    (np.float64, 3, 1024, 200003, 20),
+    (np.float64, 3, 5000, 300007, 40),
+    (np.float64, 2, 70000, 500000, 60),
+    (np.float32, 2, 3000, 400001, 10),
+    (np.float32, 1, 40000, 300000, 30),
+    (np.float64, 4, 2049, 100000, 200),
+]
+
+
+@pytest.mark.parametrize("dtype,K,G,n,spread", PART_CASES)
+def test_partitioned_forced_matches_oracle(R, partitioned, dtype, K, G, n, spread):
+    rng = np.random.default_rng(7 * n + G)
+    keys = rng.integers(0, G, n, dtype=np.int32)
+    vals = mixed_values(rng, n, dtype, spread)
+    got = gpu_groupby(R, keys, vals, G, K)
+    assert R.last_path() == 1
+    assert_bits_equal(got, oracle_groupby(keys, vals, G, K))
+
+
+@pytest.mark.parametrize("G", [5000, 1 << 17])
+def test_partitioned_auto_above_onchip_capacity(R, G):
+    rng = np.random.default_rng(G)
+    n = 1 << 20
+    keys = rng.integers(0, G, n, dtype=np.int32)
+    vals = mixed_values(rng, n, np.float64, 25)
+    got = gpu_groupby(R, keys, vals, G, 3)
+    assert R.last_path() == 1
+    assert_bits_equal(got, oracle_groupby(keys, vals, G, 3))
+
+
+def test_partitioned_skew_multi_item_partitions(R, partitioned):
+    # Zipf over 2^16 groups: the first partitions hold many work items of 2^16 rows
+    keys, vals = synth.generate_chunked(3, 1 << 21, 1 << 16)
+    got = gpu_groupby(R, keys, vals, 1 << 16, 2)
+    assert_bits_equal(got, oracle_groupby(keys, vals, 1 << 16, 2))
+
+
+def test_partitioned_empty_partitions_and_groups(R, partitioned):
+    G = 1 << 20
+    rng = np.random.default_rng(3)
+    keys = np.concatenate([rng.integers(5000, 6000, 50000), rng.integers(900000, 900100, 50000)]).astype(np.int32)
+    vals = mixed_values(rng, keys.size, np.float64, 30)
+    got = gpu_groupby(R, keys, vals, G, 3)
+    assert_bits_equal(got, oracle_groupby(keys, vals, G, 3))
+    out = gpu_groupby(R, np.zeros(0, np.int32), np.zeros(0), G, 3)
+    assert out.tobytes() == np.zeros(G).tobytes()
+
+
+def test_partitioned_accumulator_deposits(R, partitioned):
+    G = 9000
+    rng = np.random.default_rng(4)
+    keys = rng.integers(0, G, 600000, dtype=np.int32)
+    vals = mixed_values(rng, keys.size, np.float64, 40)
+    a = R.Accumulator(G, 3, R.F64)
+    for c0, c1 in ((0, 100000), (100000, 100001), (100001, 600000)):
+        a.deposit(dev(keys[c0:c1]), dev(vals[c0:c1]))
+    rc, ref, st = O.groupby_sum(keys, vals, G, 3, with_state=True)
+    assert_bits_equal(a.finalize().cpu().numpy(), ref)
+    assert a.export().cpu().numpy().reshape(G, 6).tobytes() == st.tobytes()
+
+
+def test_partitioned_errors(R, partitioned):
+    keys = np.zeros(100000, np.int32)
+    vals = np.ones(100000)
+    keys[99999] = 70000
+    with pytest.raises(R.ReproError) as ei:
+        gpu_groupby(R, keys, vals, 5000, 3)
+    assert ei.value.status == R.EKEY
+    keys[99999] = 1
+    vals[5] = np.nan
+    with pytest.raises(R.ReproError) as ei:
+        gpu_groupby(R, keys, vals, 5000, 3)
+    assert ei.value.status == R.EDOM
