@@ -1,0 +1,130 @@
+"""Multi-rank exchange on CPU: world_size 2 over gloo.
+
+`paper_1802_09883_b200.dist.allreduce_state` is the host logic the bench runs
+over NCCL.  Here each rank's accumulator is a test double backed by the CPU
+oracle (state of the rank's shard) that implements the same three calls as
+the CUDA Accumulator: top_levels / window_export / window_import.  The
+combined state must equal the oracle over all rows, bit for bit, on every rank
+and for any sharding.
+"""
+import os
+import socket
+from fractions import Fraction
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import exact_ref as X
+import oracle as O
+
+FMT = {O.F64: (52, 40), O.F32: (23, 18)}
+
+
+class OracleAccumulator:
+    """Test double: the oracle's state of a shard, in integer window form."""
+
+    def __init__(self, keys, vals, G, K):
+        self.G, self.K = G, K
+        self.dtype = O.F64 if vals.dtype == np.float64 else O.F32
+        rc, _, st = O.groupby_sum(keys, vals, G, K, threads=1, with_state=True)
+        assert rc == O.OK
+        m, W = FMT[self.dtype]
+        self.k = np.zeros(G, np.int64)
+        self.T = [[0] * K for _ in range(G)]
+        for g in range(G):
+            S, C = st[g, :K], st[g, K:]
+            e0 = int(np.frexp(S[0])[1]) - 1
+            self.k[g] = e0 // W
+            for l in range(K):
+                e = e0 - W * l
+                D = Fraction(float(S[l])) - Fraction(3, 2) * Fraction(2) ** e
+                u = Fraction(2) ** (e - m)
+                self.T[g][l] = int(D / u) + int(C[l]) * (1 << (m - 2))
+
+    def top_levels(self):
+        return torch.tensor(self.k, dtype=torch.int32)
+
+    def window_export(self, k_global):
+        kg = k_global.numpy()
+        out = np.zeros((self.G, self.K, 2), np.int64)
+        for g in range(self.G):
+            sh = int(kg[g]) - int(self.k[g])
+            assert sh >= 0
+            T = [0] * sh + self.T[g][: self.K - sh] if sh < self.K else [0] * self.K
+            for l in range(self.K):
+                out[g, l, 0] = T[l] & 0xFFFFFFFF
+                out[g, l, 1] = T[l] >> 32
+        return torch.from_numpy(out.reshape(-1))
+
+    def window_import(self, k_global, limbs):
+        L = limbs.numpy().reshape(self.G, self.K, 2)
+        self.k = k_global.numpy().astype(np.int64)
+        self.T = [[(int(L[g, l, 1]) << 32) + int(L[g, l, 0]) for l in range(self.K)] for g in range(self.G)]
+        return self
+
+    def finalize(self):
+        bits = 64 if self.dtype == O.F64 else 32
+        return np.array([X.finalize_closed_form(int(self.k[g]), self.T[g], bits) for g in range(self.G)],
+                        dtype=np.float64 if bits == 64 else np.float32)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, keys, vals, G, K, shard, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1802_09883_b200 import dist as rdist
+        if shard == "contiguous":
+            r0, r1 = rdist.shard_rows(keys.size, world, rank)
+            k, v = keys[r0:r1], vals[r0:r1]
+        else:
+            k, v = keys[rank::world], vals[rank::world]
+        acc = OracleAccumulator(k, v, G, K)
+        rdist.allreduce_state(acc)
+        q.put((rank, acc.finalize().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dtype,K,shard", [(np.float64, 3, "contiguous"), (np.float64, 2, "strided"),
+                                           (np.float32, 2, "contiguous")])
+def test_two_rank_exchange_equals_single_oracle(dtype, K, shard):
+    rng = np.random.default_rng(11)
+    n, G = 6000, 12
+    keys = rng.integers(0, G, n, dtype=np.int32)
+    e = rng.integers(-30, 31, n)
+    vals = (rng.uniform(1, 2, n) * np.exp2(e) * rng.choice([-1, 1], n)).astype(dtype)
+    vals[:7] *= 2.0 ** 50 if dtype == np.float64 else 2.0 ** 20  # rank 0 needs higher windows
+    rc, ref = O.groupby_sum(keys, vals, G, K)
+    assert rc == O.OK
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, keys, vals, G, K, shard, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0] == res[1] == ref.tobytes()
+
+
+def test_shard_rows_cover_everything():
+    from paper_1802_09883_b200 import dist as rdist
+    for n in (0, 1, 7, 1000):
+        for world in (1, 2, 3, 8):
+            spans = [rdist.shard_rows(n, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))

@@ -1,0 +1,89 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (repro_groupby_sum_async with a caller workspace on the current
+stream).  Config 1 is compared with the oracle on every group; configs 2 and 3
+(2^28 rows) on sampled groups, which the oracle computes one by one
+(orc_groupby_sum_select), always including the extreme ones."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+from paper_1802_09883_b200 import synth  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1802_09883_b200 as R
+    return R
+
+
+def run_async(R, keys, vals, G, K):
+    dt = R.F64 if vals.dtype == np.float64 else R.F32
+    k = torch.from_numpy(keys).cuda()
+    v = torch.from_numpy(vals).cuda()
+    out = torch.empty(G, dtype=v.dtype, device="cuda")
+    st = torch.full((1,), 99, dtype=torch.int32, device="cuda")
+    ws = R.make_workspace(keys.size, G, K, dt)
+    R.groupby_sum_async(k, v, G, K, out, ws, st)
+    torch.cuda.synchronize()
+    assert st.item() == 0
+    res = out.cpu().numpy()
+    del k, v, ws
+    torch.cuda.empty_cache()
+    return res
+
+
+def test_config1_full_size_all_groups(R):
+    keys, vals = synth.generate_chunked(1, 1 << 27, 1024)
+    got = run_async(R, keys, vals, 1024, 3)
+    rc, ref = O.groupby_sum(keys, vals, 1024, 3)
+    assert rc == O.OK
+    assert got.tobytes() == ref.tobytes()
+
+
+def test_config2_top_group_count_sampled(R):
+    G = 1 << 24
+    keys, vals = synth.generate_chunked(2, 1 << 28, G)
+    got = run_async(R, keys, vals, G, 3)
+    assert R.last_path() == 1
+    rng = np.random.default_rng(2)
+    sel = np.unique(np.concatenate([[0, 1, G // 2, G - 1], rng.integers(0, G, 400)])).astype(np.int32)
+    rc, ref = O.groupby_sum_select(keys, vals, G, 3, sel)
+    assert rc == O.OK
+    assert got[sel].tobytes() == ref.tobytes()
+    # groups never drawn are exactly +0.0
+    counts = np.bincount(keys, minlength=G)
+    empty = np.nonzero(counts == 0)[0][:1000]
+    assert np.all(got[empty].view(np.uint64) == 0)
+
+
+def test_config3_zipf_fp32_sampled(R):
+    G = 1 << 20
+    keys, vals = synth.generate_chunked(3, 1 << 28, G)
+    got = run_async(R, keys, vals, G, 2)
+    rng = np.random.default_rng(3)
+    sel = np.unique(np.concatenate([np.arange(8), [G - 1], rng.integers(0, G, 300)])).astype(np.int32)
+    rc, ref = O.groupby_sum_select(keys, vals, G, 2, sel)
+    assert rc == O.OK
+    assert got[sel].tobytes() == ref.tobytes()
+
+
+def test_config1_sharded_exchange_matches(R):
+    # 4 emulated ranks on one GPU through the integer window exchange
+    keys, vals = synth.generate_chunked(1, 1 << 24, 1024)
+    ref = run_async(R, keys, vals, 1024, 3)
+    accs = []
+    for r in range(4):
+        a = R.Accumulator(1024, 3, R.F64)
+        a.deposit(torch.from_numpy(keys[r::4]).cuda(), torch.from_numpy(vals[r::4]).cuda())
+        accs.append(a)
+    kg = accs[0].top_levels()
+    for a in accs[1:]:
+        kg = torch.maximum(kg, a.top_levels())
+    limbs = sum(a.window_export(kg) for a in accs)
+    accs[0].window_import(kg, limbs)
+    assert accs[0].finalize().cpu().numpy().tobytes() == ref.tobytes()
