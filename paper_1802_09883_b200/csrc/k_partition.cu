@@ -180,15 +180,15 @@ __global__ void __launch_bounds__(1024) k_part_plan(const int64_t *ptot, int P, 
     }
 }
 
+// Direct scatter (one 32-bit shared cursor per partition): best when there
+// are very few partitions (runs are long anyway) or too many to stage.
 template <typename V>
 __global__ void __launch_bounds__(HIST_TPB)
-k_part_scatter(const int32_t *__restrict__ keys, const V *__restrict__ vals, int64_t n, int32_t G, int P,
-               int64_t chunk, const uint32_t *hist, const int64_t *base, int32_t *pkeys, V *pvals) {
-    // next output row of each partition for this block (n < 2^32, so a 32-bit
-    // shared atomic serves as the cursor; 64-bit ones are CAS loops on sm_100a)
-    extern __shared__ uint32_t cursor[];
+k_part_scatter_direct(const int32_t *__restrict__ keys, const V *__restrict__ vals, int64_t n, int32_t G, int P,
+                      int64_t chunk, const uint32_t *hist, const int64_t *base, int32_t *pkeys, V *pvals) {
+    extern __shared__ uint32_t cursor_d[];
     for (int p = threadIdx.x; p < P; p += HIST_TPB)
-        cursor[p] = (uint32_t)(base[p] + hist[(size_t)blockIdx.x * P + p]);
+        cursor_d[p] = (uint32_t)(base[p] + hist[(size_t)blockIdx.x * P + p]);
     __syncthreads();
     const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);  // r0 % 4 == 0
     const int64_t v1 = r0 + ((r1 - r0) & ~(int64_t)3);
@@ -201,7 +201,7 @@ k_part_scatter(const int32_t *__restrict__ keys, const V *__restrict__ vals, int
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             if ((uint32_t)kk[j] >= (uint32_t)G) continue;
-            const uint32_t pos = atomicAdd(&cursor[kk[j] >> PART_LOG_GP], 1u);
+            const uint32_t pos = atomicAdd(&cursor_d[kk[j] >> PART_LOG_GP], 1u);
             pkeys[pos] = kk[j] & (PART_GP - 1);
             pvals[pos] = vv[j];
         }
@@ -209,9 +209,103 @@ k_part_scatter(const int32_t *__restrict__ keys, const V *__restrict__ vals, int
     for (int64_t r = v1 + threadIdx.x; r < r1; r += HIST_TPB) {
         const int k = __ldg(keys + r);
         if ((uint32_t)k >= (uint32_t)G) continue;
-        const uint32_t pos = atomicAdd(&cursor[k >> PART_LOG_GP], 1u);
+        const uint32_t pos = atomicAdd(&cursor_d[k >> PART_LOG_GP], 1u);
         pkeys[pos] = k & (PART_GP - 1);
         pvals[pos] = __ldg(vals + r);
+    }
+}
+
+// Scatter with tile-local sorting: each tile of SC_TILE rows is first grouped
+// by partition in shared memory (rank from a shared histogram, offsets from a
+// block scan), then written out so that consecutive threads store consecutive
+// rows of the same partition (coalesced runs instead of one line per lane).
+constexpr int SC_TPB = 512;
+constexpr int SC_R = 8;
+constexpr int SC_TILE = SC_TPB * SC_R;
+
+template <typename V>
+struct ScatterSmem {
+    // [P] per-partition: next global row of this block, tile count, tile start
+    static size_t bytes(int P) { return (size_t)12 * P + 64 * 4 + (size_t)SC_TILE * (sizeof(V) + 4 + 2) + 64; }
+};
+
+template <typename V>
+__global__ void __launch_bounds__(SC_TPB)
+k_part_scatter(const int32_t *__restrict__ keys, const V *__restrict__ vals, int64_t n, int32_t G, int P,
+               int64_t chunk, const uint32_t *hist, const int64_t *base, int32_t *pkeys, V *pvals) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    uint32_t *cursor = reinterpret_cast<uint32_t *>(sm);  // [P] global row (n < 2^32)
+    uint32_t *tcnt = cursor + P;                           // [P] rows of the tile per partition
+    uint32_t *tstart = tcnt + P;                           // [P] tile-local start
+    uint32_t *wsum = tstart + P;                           // [32] scan scratch
+    V *sval = reinterpret_cast<V *>(sm + (((size_t)12 * P + 64 * 4 + 15) & ~(size_t)15));
+    int32_t *skey = reinterpret_cast<int32_t *>(sval + SC_TILE);
+    uint16_t *spart = reinterpret_cast<uint16_t *>(skey + SC_TILE);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int p = tid; p < P; p += SC_TPB) {
+        cursor[p] = (uint32_t)(base[p] + hist[(size_t)blockIdx.x * P + p]);
+        tcnt[p] = 0;
+    }
+    __syncthreads();
+    const int cper = (P + SC_TPB - 1) / SC_TPB;
+    const int s0 = min(tid * cper, P), s1 = min(s0 + cper, P);
+    const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);
+    for (int64_t tb = r0; tb < r1; tb += SC_TILE) {
+        int kk[SC_R], pp[SC_R];
+        uint32_t rk[SC_R];
+        V vv[SC_R];
+#pragma unroll
+        for (int i = 0; i < SC_R; ++i) {
+            const int64_t r = tb + (int64_t)i * SC_TPB + tid;
+            kk[i] = -1;
+            if (r < r1) {
+                kk[i] = __ldg(keys + r);
+                vv[i] = __ldg(vals + r);
+            }
+            pp[i] = (uint32_t)kk[i] < (uint32_t)G ? (kk[i] >> PART_LOG_GP) : -1;
+            rk[i] = pp[i] >= 0 ? atomicAdd(&tcnt[pp[i]], 1u) : 0u;
+        }
+        __syncthreads();
+        // exclusive scan of the tile counts over the partitions
+        uint32_t local = 0;
+        for (int p = s0; p < s1; ++p) { tstart[p] = local; local += tcnt[p]; }
+        uint32_t incl = local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        uint32_t pre = incl - local;
+        for (int w = 0; w < warp; ++w) pre += wsum[w];
+        for (int p = s0; p < s1; ++p) tstart[p] += pre;
+        __syncthreads();
+        const uint32_t nvalid = wsum[SC_TPB / 32 - 1] + 0;  // total rows of the tile with a valid key
+        uint32_t total = 0;
+        for (int w = 0; w < SC_TPB / 32; ++w) total += wsum[w];
+        (void)nvalid;
+#pragma unroll
+        for (int i = 0; i < SC_R; ++i) {
+            if (pp[i] < 0) continue;
+            const uint32_t q = tstart[pp[i]] + rk[i];
+            sval[q] = vv[i];
+            skey[q] = kk[i] & (PART_GP - 1);
+            spart[q] = (uint16_t)pp[i];
+        }
+        __syncthreads();
+        for (uint32_t q = tid; q < total; q += SC_TPB) {
+            const int p = spart[q];
+            const uint32_t pos = cursor[p] + (q - tstart[p]);
+            pkeys[pos] = skey[q];
+            pvals[pos] = sval[q];
+        }
+        __syncthreads();
+        for (int p = s0; p < s1; ++p) {
+            cursor[p] += tcnt[p];
+            tcnt[p] = 0;
+        }
+        __syncthreads();
     }
 }
 
@@ -334,11 +428,10 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
     const Plan pl = make_plan(n, G);
     PartWs w = carve(ws, n, G, K, DT, pl);
     if (w.bytes > ws_bytes) return -1;
-    const size_t hsm = 4 * (size_t)pl.P, ssm = 4 * (size_t)pl.P;  // one 32-bit counter per partition
-    if (ssm > (size_t)device_props().smem_optin) return -1;
+    const size_t hsm = 4 * (size_t)pl.P, ssm = ScatterSmem<V>::bytes(pl.P);
+    if (hsm > (size_t)device_props().smem_optin) return -1;
     if (n > 0) {
         cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-        cudaFuncSetAttribute(k_part_scatter<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
         int tk = trace_begin(st);
         k_part_hist<<<pl.B, HIST_TPB, hsm, st>>>(keys, n, G, pl.P, pl.chunk, w.hist, status);
         trace_end(tk, "part_hist", st);
@@ -356,8 +449,15 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
     ++*launches;
     if (n > 0) {
         int ts = trace_begin(st);
-        k_part_scatter<V><<<pl.B, HIST_TPB, ssm, st>>>(keys, (const V *)vals, n, G, pl.P, pl.chunk, w.hist, w.base,
-                                                       w.pkeys, (V *)w.pvals);
+        if (pl.P > 8 && pl.P <= 4096) {
+            cudaFuncSetAttribute(k_part_scatter<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+            k_part_scatter<V><<<pl.B, SC_TPB, ssm, st>>>(keys, (const V *)vals, n, G, pl.P, pl.chunk, w.hist,
+                                                         w.base, w.pkeys, (V *)w.pvals);
+        } else {
+            cudaFuncSetAttribute(k_part_scatter_direct<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+            k_part_scatter_direct<V><<<pl.B, HIST_TPB, hsm, st>>>(keys, (const V *)vals, n, G, pl.P, pl.chunk,
+                                                                  w.hist, w.base, w.pkeys, (V *)w.pvals);
+        }
         trace_end(ts, "part_scatter", st);
         ++*launches;
         // per-partition tables: Gp = 1024 groups, level sums in registers
@@ -386,8 +486,8 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
 
 }  // namespace
 
-// one partitioning pass: the histogram / scatter kernels keep one 32-bit
-// counter per partition in shared memory
+// one partitioning pass: histogram and direct scatter keep one 32-bit counter
+// per partition in shared memory
 int partition_max_groups(int, int) {
     const int64_t parts = (int64_t)device_props().smem_optin / 4;
     return (int)std::min<int64_t>(parts * PART_GP, (int64_t)1 << 30);
