@@ -45,7 +45,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-shared", "-I", os.path.join(ROOT, "include"),
            "-I", CSRC, *sources(), "-o", target + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
-    with open(os.path.join(LIBDIR, "build.log"), "w") as fh:
+    log = os.path.join(LIBDIR, "build.log") if out is None else target + ".log"
+    with open(log, "w") as fh:
         fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
     if res.returncode != 0:
         sys.stderr.write(res.stdout + res.stderr)

@@ -132,23 +132,29 @@ struct OnchipWs {
     size_t zero_bytes;  // bytes from flags to the end of slots (one memset)
 };
 
-size_t onchip_ws_bytes(int32_t G, int32_t K, int32_t dt) {
+size_t onchip_zero_bytes(int32_t G, int32_t K, int32_t dt) {
     return ALIGN + align_up(sizeof(int32_t) * (size_t)G) +
            align_up(sizeof(unsigned long long) * 2 * (size_t)G * slot_count(dt, K));
 }
 
-OnchipWs carve_onchip(void *ws, int32_t G, int32_t K, int32_t dt) {
+size_t onchip_ws_bytes(int64_t n, int32_t G, int32_t K, int32_t dt) {
+    (void)n;
+    return onchip_zero_bytes(G, K, dt);
+}
+
+OnchipWs carve_onchip(void *ws, int64_t n, int32_t G, int32_t K, int32_t dt) {
     OnchipWs w;
     char *p = (char *)ws;
     w.flags = (uint32_t *)p;
     w.kglob = (int32_t *)(p + ALIGN);
     w.slots = (unsigned long long *)(p + ALIGN + align_up(sizeof(int32_t) * (size_t)G));
-    w.zero_bytes = onchip_ws_bytes(G, K, dt);
+    w.zero_bytes = onchip_zero_bytes(G, K, dt);
+    (void)n;
     return w;
 }
 
 size_t ws_bytes_for(int path, int64_t n, int32_t G, int32_t K, int32_t dt) {
-    if (path == 0) return onchip_ws_bytes(G, K, dt);
+    if (path == 0) return onchip_ws_bytes(n, G, K, dt);
     return ALIGN + partition_workspace_bytes(n, G, K, dt);
 }
 
@@ -191,7 +197,7 @@ int enqueue_groupby(const int32_t *keys, const void *vals, int64_t n, int32_t G,
     if (path < 0) return REPRO_EINVAL;
     if (ws_bytes < ws_bytes_for(path, n, G, K, dt)) return REPRO_ENOMEM;
     if (path == 0) {
-        OnchipWs w = carve_onchip(ws, G, K, dt);
+        OnchipWs w = carve_onchip(ws, n, G, K, dt);
         *flags_out = w.flags;
         if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
         int rc = timed("onchip_accumulate", st, [&] {
@@ -385,7 +391,7 @@ int repro_groupby_sum_host(const int32_t *keys_host, const void *vals_host, int6
         if (!pinned_input)
             for (int b = 0; b < nb; ++b) CK(cudaMallocHost(&pin[b], chunk_bytes));
         if (path == 0) {
-            OnchipWs w = carve_onchip(ws, n_groups, fold, dtype);
+            OnchipWs w = carve_onchip(ws, n, n_groups, fold, dtype);
             CK(cudaMemsetAsync(ws, 0, w.zero_bytes, ks));
             int c = 0;
             for (int64_t r0 = 0; r0 < n; r0 += CH, ++c) {

@@ -31,9 +31,15 @@
 #include <algorithm>
 #include <cstdlib>
 
+#ifndef ONCHIP_TMA
+#define ONCHIP_TMA 1
+#endif
+
 namespace repro {
 
-template <int DT, int K, bool REGTOT>
+static int onchip_variant();
+
+template <int DT, int K, bool REGTOT, bool TMA>
 __global__ void __launch_bounds__(256, ONCHIP_MINBLOCKS)
 k_onchip_accumulate(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals,
                     int64_t n, int32_t G, int64_t chunk, int32_t *__restrict__ kglob,
@@ -43,7 +49,7 @@ k_onchip_accumulate(const int32_t *__restrict__ keys, const typename Fmt<DT>::V 
     const int64_t row1 = min(n, row0 + chunk);
     uint32_t flags = 0;
     PubArgs out{kglob, slots, nullptr, nullptr};
-    accumulate_range<DT, K, REGTOT, 0>(keys, vals, row0, row1, G, smem, flags, out);
+    accumulate_range<DT, K, REGTOT, 0, TMA>(keys, vals, row0, row1, G, smem, flags, out);
     flags = __reduce_or_sync(0xffffffffu, flags);
     if ((threadIdx.x & 31) == 0 && flags) atomicOr(status, flags);
 }
@@ -52,15 +58,20 @@ template <int DT, int K>
 int launch_onchip(const int32_t *keys, const void *vals, int64_t n, int32_t G, int32_t *kglob,
                   unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches) {
     using Cfg = OnchipCfg<DT, K>;
-    const bool regtot = G <= 4 * Cfg::TPB && G <= ONCHIP_REGTOT_MAXG;  // level sums in registers
-    auto kern = regtot ? k_onchip_accumulate<DT, K, true> : k_onchip_accumulate<DT, K, false>;
-    const size_t smem = onchip_smem_bytes<DT, K>(G) - (regtot ? (size_t)8 * K * G : 0);
+    const bool regtot = G <= Cfg::REG_GQ;  // level sums in registers
+    // TMA-fed ring when both columns are 16-byte aligned and the ring fits
+    const size_t table = onchip_smem_bytes<DT, K>(G, regtot);
+    const bool tma = ONCHIP_TMA && onchip_variant() != 3 && ((((uintptr_t)keys) | ((uintptr_t)vals)) & 15) == 0 &&
+                     table + onchip_ring_bytes<DT, K>() <= (size_t)device_props().smem_optin;
+    auto kern = regtot ? (tma ? k_onchip_accumulate<DT, K, true, true> : k_onchip_accumulate<DT, K, true, false>)
+                       : (tma ? k_onchip_accumulate<DT, K, false, true> : k_onchip_accumulate<DT, K, false, false>);
+    const size_t smem = table + (tma ? onchip_ring_bytes<DT, K>() : 0);
     if (smem > (size_t)device_props().smem_optin) return -1;
-    static thread_local int configured_smem[2][5][2] = {};
-    if (configured_smem[DT][K][regtot] < (int)smem) {
+    static thread_local int configured_smem[2][5][2][2] = {};
+    if (configured_smem[DT][K][regtot][tma] < (int)smem) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
             return -2;
-        configured_smem[DT][K][regtot] = (int)smem;
+        configured_smem[DT][K][regtot][tma] = (int)smem;
     }
     if (n == 0) return 0;
     int per_sm = 0;
@@ -81,26 +92,30 @@ int launch_onchip(const int32_t *keys, const void *vals, int64_t n, int32_t G, i
 }
 
 int atomic_max_groups(int K, int DT) {
+    // largest G whose table (level sums in shared memory, G rounded to 4)
+    // fits; the register-sum kernel covers G <= REG_GQ in less space
     const size_t cap = (size_t)device_props().smem_optin;
-    size_t per = (size_t)(8 * K + 4 * ((K * (DT == 1 ? 2 : 1)) | 1) + 8);  // == onchip_smem_bytes / G
-    return (int)((cap - 16) / per);
+    const size_t cw = (size_t)K * (DT == 1 ? 2 : 1);
+    const size_t per = 8 * K + 4 * cw + 8;  // onchip_table_bytes = GQ * per + 64
+    return (int)(((cap - 64 - 127) / per) & ~(size_t)3);
 }
 
-// variant: 0 = auto, 1 = atomic, 2 = sorted.
+// variant: 0 = auto, 1 = atomic (TMA-fed where the columns are 16-B aligned),
+// 2 = sorted, 3 = atomic with register loads only.
 // Initialised from REPRO_ONCHIP_VARIANT, settable through the C-ABI.
 static int g_variant = -1;
 static int onchip_variant() {
     if (g_variant < 0) {
         const char *e = getenv("REPRO_ONCHIP_VARIANT");
-        g_variant = (e && e[0] == 'a') ? 1 : (e && e[0] == 's') ? 2 : 0;
+        g_variant = (e && e[0] == 'a') ? 1 : (e && e[0] == 's') ? 2 : (e && e[0] == 'r') ? 3 : 0;
     }
     return g_variant;
 }
-void set_onchip_variant(int v) { g_variant = (v >= 0 && v <= 2) ? v : 0; }
+void set_onchip_variant(int v) { g_variant = (v >= 0 && v <= 3) ? v : 0; }
 
 int onchip_max_groups(int K, int DT) {
     const int v = onchip_variant();
-    if (v == 1) return atomic_max_groups(K, DT);
+    if (v == 1 || v == 3) return atomic_max_groups(K, DT);
     if (v == 2) return sorted_max_groups(K, DT);
     return std::max(atomic_max_groups(K, DT), sorted_max_groups(K, DT));
 }

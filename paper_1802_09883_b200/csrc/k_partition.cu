@@ -462,7 +462,7 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
         ++*launches;
         // per-partition tables: Gp = 1024 groups, level sums in registers
         auto kern = k_part_accumulate<DT, K>;
-        const size_t smem = onchip_smem_bytes<DT, K>(PART_GP) - (size_t)8 * K * PART_GP;
+        const size_t smem = onchip_smem_bytes<DT, K>(PART_GP, true);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);

@@ -8,55 +8,126 @@
 namespace repro {
 
 #ifndef ONCHIP_R64
-#define ONCHIP_R64 15
+#define ONCHIP_R64 7
+#endif
+#ifndef ONCHIP_R32
+#define ONCHIP_R32 15
 #endif
 #ifndef ONCHIP_MINBLOCKS
 #define ONCHIP_MINBLOCKS 2
 #endif
-#ifndef ONCHIP_REGTOT_MAXG
-#define ONCHIP_REGTOT_MAXG 1024
+#ifndef ONCHIP_STAGES
+#define ONCHIP_STAGES 3
+#endif
+#ifndef ONCHIP_FAST
+#define ONCHIP_FAST 1
+#endif
+#ifndef ONCHIP_SKIPZ
+#define ONCHIP_SKIPZ 1
+#endif
+#ifndef ONCHIP_NB
+#define ONCHIP_NB 4
 #endif
 
+// Table geometry.  The limb counters are WORD-MAJOR: counter w of group g is
+// cnt[w * GQ + g], with GQ the group count rounded up to a multiple of 4 (1024
+// when the level sums live in registers, so every address offset is an
+// immediate).  A warp's shared atomic on one counter position w then hits
+// bank (g + const) mod 32 -- random groups spread over all banks -- while the
+// fold reads and clears four groups' counters with one 128-bit access.
 template <int DT, int K>
 struct OnchipCfg {
     static constexpr int TPB = 256;
-    static constexpr int R = (DT == 1) ? ONCHIP_R64 : 16;  // rows per thread per tile
-    static constexpr int TILE = TPB * R;           // 3840 / 4096
-    // limb counters accept at most LIMIT rows' worth of digits between folds
+    static constexpr int R = (DT == 1) ? ONCHIP_R64 : ONCHIP_R32;  // rows per thread per tile
+    static constexpr int TILE = TPB * R;
+    // limb counters accept at most LIMIT rows' worth of digits between folds:
+    // balanced binary64 limbs have |limb| <= 2^19 (4095 * 2^19 < 2^31), binary32
+    // digits |d| <= 2^17 (16383 * 2^17 < 2^31)
     static constexpr int LIMIT = (DT == 1) ? 4095 : 16383;
     static constexpr int LIMBS = Fmt<DT>::LIMBS;
     static constexpr int CW = K * LIMBS;  // 32-bit counters per group
-    // group-major rows of CWP words; an odd stride spreads random groups over
-    // all 32 banks (stride 6 would use only 16 and double the conflicts)
-    static constexpr int CWP = CW | 1;
+    static constexpr int REG_GQ = 4 * TPB;  // groups covered when level sums are in registers (4 per thread)
     static_assert(TILE <= LIMIT, "tile larger than limb headroom");
 };
 
+// groups per counter row: REG_GQ with register level sums, else G rounded to 4
 template <int DT, int K>
-size_t onchip_smem_bytes(int G) {
+__host__ __device__ inline int onchip_gq(int G, bool regtot) {
+    return regtot ? OnchipCfg<DT, K>::REG_GQ : (G + 3) & ~3;
+}
+
+// Shared memory of one block: [level sums int64 [GQ][K] (unless REGTOT)]
+// [counters u32 [CW][GQ]] [ktop_cur [GQ]] [ktop_next [GQ]] [16 words misc],
+// then, for the TMA-fed kernel, 128 bytes of mbarriers and a ring of STAGES
+// tiles of keys + values.
+template <int DT, int K>
+__host__ __device__ inline size_t onchip_table_bytes(int G, bool regtot = false) {
     using C = OnchipCfg<DT, K>;
-    return (size_t)G * (8 * K + 4 * C::CWP + 8) + 16;
+    const size_t gq = (size_t)onchip_gq<DT, K>(G, regtot);
+    return gq * ((regtot ? 0 : 8 * K) + 4 * C::CW + 8) + 64;
+}
+template <int DT, int K>
+constexpr size_t onchip_ring_bytes() {
+    using C = OnchipCfg<DT, K>;
+    return 128 + (size_t)ONCHIP_STAGES * C::TILE * (4 + sizeof(typename Fmt<DT>::V));
+}
+template <int DT, int K>
+size_t onchip_smem_bytes(int G, bool regtot = false, bool tma = false) {
+    return ((onchip_table_bytes<DT, K>(G, regtot) + 127) & ~(size_t)127) + (tma ? onchip_ring_bytes<DT, K>() : 0);
+}
+
+// ---- TMA bulk copies (cp.async.bulk) and mbarriers -------------------------
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}"
+        :: "r"(bar), "r"(parity) : "memory");
+}
+// global -> shared bulk copy of `bytes` (multiple of 16, both 16-B aligned),
+// completing on mbarrier `bar`
+__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        :: "r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // Limbs of one row's K digits, computed from the bits (common.cuh digits_of
-// written out so that no 64-bit integer arithmetic is needed):
-//   binary64: t = x (+) 1.5*2^52 has low word = low word of the digit d and
-//   high word = high word of d + 0x43380000; limbs are d mod 2^20 and d >> 20
-//   (a funnel shift of the two words).  binary32: one int32 limb per level.
+// written out so that no 64-bit integer arithmetic is needed).
+//   binary64: the extractor is M' = 1.5*2^52 + 2^19, so t = x (+) M' has the
+//   bits of 1.5*2^52 plus (d + 2^19) (an integer shift of the extractor does
+//   not change the rounding of x, and t (-) M' = d exactly).  The digit is split
+//   into BALANCED limbs d = lo + hi*2^20 with lo = ((d + 2^19) mod 2^20) - 2^19
+//   in [-2^19, 2^19) and hi = floor((d + 2^19) / 2^20) in [-2^19, 2^19]: a
+//   digit with |d| < 2^19 has hi == 0 whatever its sign, a multiple of 2^20 has
+//   lo == 0 (deposit_batch skips counters that a whole warp leaves at zero).
+//   hi is a funnel shift of the two words of t (the exponent field of t
+//   contributes exactly 0x80000000 to it).
+//   binary32: one int32 limb per level (|d| <= 2^17).
 // `s` is the row's value already scaled to units of the top level's ulp.
 template <int DT, int K>
 __device__ __forceinline__ void row_limbs(typename Fmt<DT>::V s, uint32_t (&lo)[K], uint32_t (&hi)[K]) {
     if (DT == 1) {
-        const double M = 6755399441055744.0;       // 1.5 * 2^52
-        const double T40 = 1099511627776.0;        // 2^40
+        const double M = 6755399441055744.0 + 524288.0;  // 1.5 * 2^52 + 2^19
+        const double T40 = 1099511627776.0;              // 2^40
 #pragma unroll
         for (int l = 0; l < K; ++l) {
             const double x = __hiloint2double(__double2hiint(s), __double2loint(s) | 1);
             const double t = __dadd_rn(x, M);
             const uint32_t tlo = (uint32_t)__double2loint(t);
-            const uint32_t dhi = (uint32_t)__double2hiint(t) - 0x43380000u;
-            lo[l] = tlo & 0xFFFFFu;
-            hi[l] = __funnelshift_r(tlo, dhi, 20);
+            const uint32_t thi = (uint32_t)__double2hiint(t);
+            lo[l] = (tlo & 0xFFFFFu) - 0x80000u;
+            hi[l] = __funnelshift_r(tlo, thi, 20) ^ 0x80000000u;
             if (l + 1 < K) s = __dmul_rn(__dsub_rn(s, __dsub_rn(t, M)), T40);
         }
     } else {
@@ -73,91 +144,215 @@ __device__ __forceinline__ void row_limbs(typename Fmt<DT>::V s, uint32_t (&lo)[
     }
 }
 
+// 32-bit shared-memory reduction (ATOMS.ADD without return) at a shared-window
+// address.
+__device__ __forceinline__ void red_shared(uint32_t a, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
+}
+
+// Generic deposit of one row: digits under the window whose scale is already
+// applied to s; key < 0 deposits nothing.  UNIFORM (small G): a warp whose
+// lanes all hold one group reduces with REDUX first.
 template <int DT, int K, bool UNIFORM>
-__device__ __forceinline__ void deposit_row(uint32_t *cnt, int key, typename Fmt<DT>::V s, int lane) {
+__device__ __forceinline__ void deposit_row(uint32_t *cnt, int gq, int key, typename Fmt<DT>::V s, int lane) {
     using Cfg = OnchipCfg<DT, K>;
     uint32_t lo[K], hi[K];
     row_limbs<DT, K>(s, lo, hi);
     if (UNIFORM) {
-        // small G: when the whole warp holds one group, reduce with a uniform REDUX first
         const int k0 = __shfl_sync(0xffffffffu, key, 0);
         if (__all_sync(0xffffffffu, key == k0 && key >= 0)) {
-            uint32_t *p = cnt + (size_t)k0 * Cfg::CWP;
+            uint32_t *p = cnt + k0;
 #pragma unroll
             for (int l = 0; l < K; ++l) {
                 const uint32_t a = __reduce_add_sync(0xffffffffu, lo[l]);
                 if (Cfg::LIMBS == 2) {
                     const uint32_t b = __reduce_add_sync(0xffffffffu, hi[l]);
-                    if (lane == 0) { atomicAdd(p + 2 * l, a); atomicAdd(p + 2 * l + 1, b); }
+                    if (lane == 0) {
+                        atomicAdd(p + (size_t)(2 * l) * gq, a);
+                        atomicAdd(p + (size_t)(2 * l + 1) * gq, b);
+                    }
                 } else if (lane == 0) {
-                    atomicAdd(p + l, a);
+                    atomicAdd(p + (size_t)l * gq, a);
                 }
             }
             return;
         }
     }
     if (key >= 0) {
-        uint32_t *p = cnt + (size_t)key * Cfg::CWP;
+        uint32_t *p = cnt + key;
 #pragma unroll
         for (int l = 0; l < K; ++l) {
             if (Cfg::LIMBS == 2) {
-                atomicAdd(p + 2 * l, lo[l]);
-                atomicAdd(p + 2 * l + 1, hi[l]);
+                atomicAdd(p + (size_t)(2 * l) * gq, lo[l]);
+                atomicAdd(p + (size_t)(2 * l + 1) * gq, hi[l]);
             } else {
-                atomicAdd(p + l, lo[l]);
+                atomicAdd(p + (size_t)l * gq, lo[l]);
             }
         }
     }
 }
 
+// Per-level extractors of the fast path for window top k: level l (ulp u,
+// the top level is l = 0) uses E_l = 1.5 * 2^m * u (+ 2^19 u for binary64's
+// balanced limbs).  x (+) E_l for an unscaled remainder x is the paper's own
+// extraction step q = (r (+) S) (-) S (Alg. 1 line 11) with S = E_l,
+// and the bits of the sum are those of 1.5 * 2^m * u plus the digit: no scaling
+// multiplies are needed.  `eb` holds the high word of 1.5 * 2^m * u shifted
+// left by 12 (binary64: removed from the funnel-shifted high limb) or the
+// bits of 1.5 * 2^m * u (binary32).
 template <int DT, int K>
-__device__ __forceinline__ int64_t counters_value(const uint32_t *c, int l) {
-    if (Fmt<DT>::LIMBS == 2) return (int64_t)c[2 * l] + (int64_t)(int32_t)c[2 * l + 1] * (int64_t)(1 << 20);
-    return (int64_t)(int32_t)c[l];
+struct Extractors {
+    typename Fmt<DT>::V e[K];
+    uint32_t eb[K];
+    __device__ __forceinline__ Extractors(int k) {
+        using F = Fmt<DT>;
+#pragma unroll
+        for (int l = 0; l < K; ++l) {
+            const int ue = F::W * (k - l) - F::m;  // log2 of the level's ulp
+            const typename F::V base = F::add(F::pow2(ue + F::m), F::pow2(ue + F::m - 1));  // 1.5 * 2^m * u
+            if (DT == 1) {
+                e[l] = F::add(base, F::pow2(ue + 19));
+                eb[l] = (uint32_t)(F::bits(base) >> 32) << 12;
+            } else {
+                e[l] = base;
+                eb[l] = (uint32_t)F::bits(base);
+            }
+        }
+    }
+};
+
+// Fast-path deposit of NB rows known to be valid (keys in range, k* <= the
+// block-uniform top): all limbs of the batch are computed first, then each
+// counter position is updated for every row of the batch unless the whole warp
+// holds zeros there (one vote per position and batch: small digits and values
+// with few significant bits leave whole counters untouched).  Counter w of
+// group g lives at shared address cbase + 4 g + w * wstride.
+template <int DT, int K, int NB>
+__device__ __forceinline__ void deposit_batch(uint32_t cbase, uint32_t wstride, const int32_t *key,
+                                              const typename Fmt<DT>::V *val, const Extractors<DT, K> &ex) {
+    using Cfg = OnchipCfg<DT, K>;
+    uint32_t lo[NB][K], hi[NB][K], a[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        a[i] = cbase + 4u * (uint32_t)key[i];
+        if (DT == 1) {
+            double r = (double)val[i];
+#pragma unroll
+            for (int l = 0; l < K; ++l) {
+                const double x = __hiloint2double(__double2hiint(r), __double2loint(r) | 1);  // reading A-1
+                const double t = __dadd_rn(x, (double)ex.e[l]);
+                const uint32_t tlo = (uint32_t)__double2loint(t);
+                const uint32_t thi = (uint32_t)__double2hiint(t);
+                lo[i][l] = (tlo & 0xFFFFFu) - 0x80000u;
+                hi[i][l] = __funnelshift_r(tlo, thi, 20) - ex.eb[l];
+                if (l + 1 < K) r = __dsub_rn(r, __dsub_rn(t, (double)ex.e[l]));
+            }
+        } else {
+            float r = (float)val[i];
+#pragma unroll
+            for (int l = 0; l < K; ++l) {
+                const float x = __uint_as_float(__float_as_uint(r) | 1u);
+                const float t = __fadd_rn(x, (float)ex.e[l]);
+                lo[i][l] = __float_as_uint(t) - ex.eb[l];
+                hi[i][l] = 0;
+                if (l + 1 < K) r = __fsub_rn(r, __fsub_rn(t, (float)ex.e[l]));
+            }
+        }
+    }
+#pragma unroll
+    for (int l = 0; l < K; ++l) {
+#pragma unroll
+        for (int h = 0; h < Cfg::LIMBS; ++h) {
+            uint32_t any = 0;
+#pragma unroll
+            for (int i = 0; i < NB; ++i) any |= h ? hi[i][l] : lo[i][l];
+            if (ONCHIP_SKIPZ == 0 || __any_sync(0xffffffffu, any != 0u)) {
+                const uint32_t off = (uint32_t)(Cfg::LIMBS * l + h) * wstride;
+#pragma unroll
+                for (int i = 0; i < NB; ++i) red_shared(a[i] + off, h ? hi[i][l] : lo[i][l]);
+            }
+        }
+    }
 }
 
-// Fold the limb counters of group g into its level sums t[] (if `fold`) and
-// demote its levels when its window top moved.
+// value of one level's counters (low and high limb counter words)
 template <int DT, int K>
-__device__ __forceinline__ void fold_group(uint32_t *__restrict__ c, int64_t (&t)[K], bool fold, int32_t *ktop_cur,
-                                           const int32_t *ktop_next, int g) {
+__device__ __forceinline__ int64_t limbs_value(uint32_t clo, uint32_t chi) {
+    if (Fmt<DT>::LIMBS == 2) return (int64_t)(int32_t)clo + (int64_t)(int32_t)chi * (int64_t)(1 << 20);
+    return (int64_t)(int32_t)clo;
+}
+template <int DT, int K>
+__device__ __forceinline__ int64_t counters_value(const uint32_t *cnt, int gq, int g, int l) {
+    if (Fmt<DT>::LIMBS == 2)
+        return limbs_value<DT, K>(cnt[(size_t)(2 * l) * gq + g], cnt[(size_t)(2 * l + 1) * gq + g]);
+    return limbs_value<DT, K>(cnt[(size_t)l * gq + g], 0u);
+}
+
+// Fold the limb counters of the four groups 4q..4q+3 into their level sums
+// t[4][K] (if `fold`: one 128-bit load and store per counter position) and
+// demote the groups whose window top moved (ktop_next > ktop_cur, PAPER.md:
+// 661-664): level sums and counters shift down by the difference, the top
+// level restarts at zero.
+template <int DT, int K>
+__device__ __forceinline__ void fold_quad(uint32_t *__restrict__ cnt, int gq, int q, int64_t (&t)[4][K], bool fold,
+                                          int32_t *ktop_cur, const int32_t *ktop_next) {
     using Cfg = OnchipCfg<DT, K>;
     if (fold) {
+        uint4 c[Cfg::CW];
 #pragma unroll
-        for (int l = 0; l < K; ++l) t[l] += counters_value<DT, K>(c, l);
+        for (int w = 0; w < Cfg::CW; ++w) {
+            uint4 *p = reinterpret_cast<uint4 *>(cnt + (size_t)w * gq) + q;
+            c[w] = *p;
+            *p = make_uint4(0u, 0u, 0u, 0u);
+        }
 #pragma unroll
-        for (int w = 0; w < Cfg::CW; ++w) c[w] = 0;
+        for (int l = 0; l < K; ++l) {
+            const uint4 a = c[Cfg::LIMBS * l];
+            const uint4 b = Cfg::LIMBS == 2 ? c[Cfg::LIMBS * l + 1] : make_uint4(0u, 0u, 0u, 0u);
+            t[0][l] += limbs_value<DT, K>(a.x, b.x);
+            t[1][l] += limbs_value<DT, K>(a.y, b.y);
+            t[2][l] += limbs_value<DT, K>(a.z, b.z);
+            t[3][l] += limbs_value<DT, K>(a.w, b.w);
+        }
     }
-    const int kn = ktop_next[g], ko = ktop_cur[g];
-    if (kn != ko) {
-        const int sh = kn - ko;
+    const int4 kn = reinterpret_cast<const int4 *>(ktop_next)[q];
+    const int4 ko = reinterpret_cast<const int4 *>(ktop_cur)[q];
+    if (kn.x != ko.x || kn.y != ko.y || kn.z != ko.z || kn.w != ko.w) {
+        const int knv[4] = {kn.x, kn.y, kn.z, kn.w}, kov[4] = {ko.x, ko.y, ko.z, ko.w};
 #pragma unroll
-        for (int r = 0; r < K; ++r) {  // sh single-level shifts (static register indices)
-            if (r < sh) {
+        for (int j = 0; j < 4; ++j) {
+            const int sh = knv[j] - kov[j];
+            if (sh == 0) continue;
+            const int g = 4 * q + j;
 #pragma unroll
-                for (int l = K - 1; l >= 1; --l) t[l] = t[l - 1];
-                t[0] = 0;
+            for (int r = 0; r < K; ++r) {  // sh single-level shifts (static register indices)
+                if (r < sh) {
+#pragma unroll
+                    for (int l = K - 1; l >= 1; --l) t[j][l] = t[j][l - 1];
+                    t[j][0] = 0;
+                }
+            }
+#pragma unroll
+            for (int l = K - 1; l >= 0; --l) {
+#pragma unroll
+                for (int b = 0; b < Cfg::LIMBS; ++b)
+                    cnt[(size_t)(l * Cfg::LIMBS + b) * gq + g] =
+                        l - sh >= 0 ? cnt[(size_t)((l - sh) * Cfg::LIMBS + b) * gq + g] : 0u;
             }
         }
-#pragma unroll
-        for (int l = K - 1; l >= 0; --l) {
-#pragma unroll
-            for (int b = 0; b < Cfg::LIMBS; ++b)
-                c[l * Cfg::LIMBS + b] = l - sh >= 0 ? c[(l - sh) * Cfg::LIMBS + b] : 0u;
-        }
-        ktop_cur[g] = kn;
+        reinterpret_cast<int4 *>(ktop_cur)[q] = kn;
     }
 }
 
 // Publish a block's level sums of group g into the absolute-level slot table.
 template <int DT, int K>
-__device__ __forceinline__ void publish_group(const uint32_t *c, const int64_t (&t)[K], int k, int g,
+__device__ __forceinline__ void publish_group(const uint32_t *cnt, int gq, const int64_t (&t)[K], int k, int g,
                                               int32_t *kglob, unsigned long long *slots) {
     constexpr int NS = Fmt<DT>::KMAX + K;
     if (k > 0) atomicMax(&kglob[g], k);
 #pragma unroll
     for (int l = 0; l < K; ++l) {
-        const int64_t T = t[l] + counters_value<DT, K>(c, l);
+        const int64_t T = t[l] + counters_value<DT, K>(cnt, gq, g, l);
         if (T != 0) {
             unsigned long long *p = slots + ((size_t)g * NS + (k - l + K - 1)) * 2;
             atomicAdd(p, (unsigned long long)(T & 0xFFFFFFFFll));
@@ -196,7 +391,7 @@ struct PubArgs {
 // One block deposits rows [row0, row1) of (keys, vals) into a fresh table of G
 // groups in shared memory (+ registers) and publishes it.  Must be entered by
 // all threads of the block; `smem` is the dynamic shared memory.
-template <int DT, int K, bool REGTOT, int MODE>
+template <int DT, int K, bool REGTOT, int MODE, bool TMA = false>
 __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ keys,
                                                  const typename Fmt<DT>::V *__restrict__ vals, int64_t row0,
                                                  int64_t row1, int32_t G, unsigned char *smem, uint32_t &flags,
@@ -204,48 +399,161 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
     using F = Fmt<DT>;
     using V = typename F::V;
     using Cfg = OnchipCfg<DT, K>;
-    constexpr int TPB = Cfg::TPB, R = Cfg::R, TILE = Cfg::TILE, CW = Cfg::CW, CWP = Cfg::CWP;
-    constexpr int NS = F::KMAX + K;  // absolute slots per group
-    constexpr int GPT = 4;           // groups per thread when the level sums live in registers
+    constexpr int TPB = Cfg::TPB, R = Cfg::R, TILE = Cfg::TILE, CW = Cfg::CW;
+    const int gq = onchip_gq<DT, K>(G, REGTOT);
+    const int nq = gq >> 2;  // group quads
 
-    int64_t *tot = reinterpret_cast<int64_t *>(smem);                    // [G][K] (unless REGTOT)
-    uint32_t *cnt = reinterpret_cast<uint32_t *>(tot + (REGTOT ? 0 : (size_t)K * G));  // [G][CWP]
-    int32_t *ktop_cur = reinterpret_cast<int32_t *>(cnt + (size_t)CWP * G);
-    int32_t *ktop_next = ktop_cur + G;
-    int32_t *kminmax = ktop_next + G;  // [0] min, [1] max of ktop_cur over the groups
+    int64_t *tot = reinterpret_cast<int64_t *>(smem);                                   // [GQ][K] (unless REGTOT)
+    uint32_t *cnt = reinterpret_cast<uint32_t *>(tot + (REGTOT ? 0 : (size_t)K * gq));  // [CW][GQ]
+    int32_t *ktop_cur = reinterpret_cast<int32_t *>(cnt + (size_t)CW * gq);
+    int32_t *ktop_next = ktop_cur + gq;
+    int32_t *kminmax = ktop_next + gq;  // [0] min, [1] max of ktop_cur over the groups
+    const uint32_t cbase = (uint32_t)__cvta_generic_to_shared(cnt);
+    const uint32_t wstride = REGTOT ? 4u * Cfg::REG_GQ : 4u * (uint32_t)gq;
 
     const int tid = threadIdx.x;
     const int lane = tid & 31;
-    int64_t treg[GPT][K];  // level sums of groups tid + j*TPB (REGTOT)
+    int64_t treg[4][K];  // level sums of groups 4 tid .. 4 tid + 3 (REGTOT)
 #pragma unroll
-    for (int j = 0; j < GPT; ++j)
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
         for (int l = 0; l < K; ++l) treg[j][l] = 0;
     if (!REGTOT)
-        for (int i = tid; i < K * G; i += TPB) tot[i] = 0;
-    for (int i = tid; i < CWP * G; i += TPB) cnt[i] = 0;
-    for (int i = tid; i < G; i += TPB) { ktop_cur[i] = 0; ktop_next[i] = 0; }
+        for (int i = tid; i < K * gq; i += TPB) tot[i] = 0;
+    for (int i = tid; i < CW * gq; i += TPB) cnt[i] = 0;
+    for (int i = tid; i < gq; i += TPB) { ktop_cur[i] = 0; ktop_next[i] = 0; }
     __syncthreads();
     // block-uniform window top: when every group has the same top `kuni`,
     // rows need no per-group lookup (the common case after the first tiles)
     int kuni = 0;
 
+    // fold all counters into the level sums, demoting moved groups
+    auto fold_all = [&](bool fold) {
+        if (REGTOT) {
+            fold_quad<DT, K>(cnt, gq, tid, treg, fold, ktop_cur, ktop_next);
+        } else {
+            for (int q = tid; q < nq; q += TPB) {
+                int64_t t[4][K];
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int l = 0; l < K; ++l) t[j][l] = tot[(size_t)(4 * q + j) * K + l];
+                fold_quad<DT, K>(cnt, gq, q, t, fold, ktop_cur, ktop_next);
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+#pragma unroll
+                    for (int l = 0; l < K; ++l) tot[(size_t)(4 * q + j) * K + l] = t[j][l];
+            }
+        }
+    };
+
     const bool small_g = G <= 32;
     int since = 0;  // rows' worth of digits in the counters since the last fold
 
-    for (int64_t base = row0; base < row1; base += TILE) {
-        const int32_t *kp = keys + base + tid;
-        const V *vp = vals + base + tid;
+    // a1: coalesced loads (immediate offsets i*TPB from one base pointer),
+    // bounds-checked, straight from global memory
+    auto load_tile = [&](int64_t b, int32_t(&k)[R], V(&v)[R]) {
+        const int32_t *kp = keys + b + tid;
+        const V *vp = vals + b + tid;
+        const int rm = (int)min((int64_t)TILE, row1 - b) - tid;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const bool in = i * TPB < rm;
+            k[i] = in ? __ldg(kp + i * TPB) : -1;
+            v[i] = in ? __ldg(vp + i * TPB) : V(0);
+        }
+    };
+    // TMA-fed variant: full tiles stream through a ring of STAGES shared
+    // buffers filled by cp.async.bulk (thread 0 issues, an mbarrier per stage
+    // completes on the byte count); tile t lives in stage t % STAGES.  A stage
+    // is refilled with tile t + STAGES right after tile t's first barrier, by
+    // which point every thread has consumed tile t's rows into registers (the
+    // level check reads every loaded register before the barrier), so
+    // STAGES - 1 tiles are always in flight while the block works.
+    constexpr int S = ONCHIP_STAGES;
+    const size_t tbytes = (onchip_table_bytes<DT, K>(G, REGTOT) + 127) & ~(size_t)127;
+    const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)tbytes;  // mbarriers, then tiles
+    auto stage_keys = [&](int st) { return ring + 128u + (uint32_t)st * (uint32_t)(TILE * (4 + sizeof(V))); };
+    auto issue = [&](int64_t t_base, int st) {  // thread 0 only; full tiles only
+        const uint32_t bar = ring + 8u * st;
+        mbar_expect_tx(bar, (uint32_t)(TILE * (4 + sizeof(V))));
+        tma_load_1d(stage_keys(st), keys + t_base, TILE * 4, bar);
+        tma_load_1d(stage_keys(st) + TILE * 4, vals + t_base, TILE * sizeof(V), bar);
+    };
+    if (TMA) {
+        if (tid == 0) {
+            for (int st = 0; st < S; ++st) mbar_init(ring + 8u * st, 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0)
+            for (int st = 0; st < S; ++st)
+                if (row0 + (int64_t)(st + 1) * TILE <= row1) issue(row0 + (int64_t)st * TILE, st);
+    }
+
+    int tile = 0;
+    for (int64_t base = row0; base < row1; base += TILE, ++tile) {
         const int rem = (int)min((int64_t)TILE, row1 - base) - tid;  // rows i*TPB < rem exist
         int32_t key[R];
         V val[R];
         int kc[R];
-        // a1: coalesced loads (immediate offsets i*TPB from one base pointer)
+        if (TMA && base + TILE <= row1) {
+            const int st = tile % S;
+            mbar_wait(ring + 8u * st, (uint32_t)((tile / S) & 1));
+            const int32_t *sk =
+                reinterpret_cast<const int32_t *>(smem + tbytes + 128 + (size_t)st * TILE * (4 + sizeof(V)));
+            const V *sv = reinterpret_cast<const V *>(sk + TILE);
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
-            const bool in = i * TPB < rem;
-            key[i] = in ? __ldg(kp + i * TPB) : -1;
-            val[i] = in ? __ldg(vp + i * TPB) : V(0);
+            for (int i = 0; i < R; ++i) { key[i] = sk[tid + i * TPB]; val[i] = sv[tid + i * TPB]; }
+        } else {
+            load_tile(base, key, val);
+        }
+        // refill this tile's stage (right after the tile's first barrier)
+        auto refill = [&]() {
+            if (TMA && tid == 0 && base + (int64_t)(S + 1) * TILE <= row1) {
+                fence_proxy_async_smem();
+                issue(base + (int64_t)S * TILE, tile % S);
+            }
+        };
+        // Fast path: when the block has a uniform window top kuni and every row
+        // of this full tile has a valid key and needs no level shift, the tile
+        // is deposited without per-row checks.  One barrier decides it for the
+        // whole block (and orders the previous tile's deposits before a fold).
+        if (ONCHIP_FAST && !small_g) {
+            int slow = kuni < 0 || rem < TILE - tid;
+            if (!slow) {
+                // k*(b) <= kuni  <=>  |b| < 2^(W kuni + W - 1 - m): compare the
+                // magnitude bits (sign shifted out); NaN/Inf fail it too
+                const uint32_t lim = (uint32_t)(F::W * kuni + F::W - 1 - F::m + F::BIAS) << (F::m % 32 + 1);
+                uint32_t hwmax = 0, kmax = 0;
+#pragma unroll
+                for (int i = 0; i < R; ++i) {
+                    uint32_t hw;
+                    if (DT == 1) hw = (uint32_t)__double2hiint((double)val[i]) << 1;
+                    else hw = __float_as_uint((float)val[i]) << 1;
+                    hwmax = max(hwmax, hw);
+                    kmax = max(kmax, (uint32_t)key[i]);
+                }
+                slow = (hwmax >= lim) | (kmax >= (uint32_t)G);
+            }
+            const int any_slow = __syncthreads_or(slow);
+            refill();
+            if (!any_slow) {
+                if (since + TILE > Cfg::LIMIT) {
+                    fold_all(true);
+                    since = 0;
+                    __syncthreads();
+                }
+                since += TILE;
+                const Extractors<DT, K> ex(kuni);
+                constexpr int NB = ONCHIP_NB < R ? ONCHIP_NB : R;
+#pragma unroll
+                for (int i0 = 0; i0 < R; i0 += NB) {
+                    if (i0 + NB <= R) deposit_batch<DT, K, NB>(cbase, wstride, key + i0, val + i0, ex);
+                    else deposit_batch<DT, K, (R % NB ? R % NB : NB)>(cbase, wstride, key + i0, val + i0, ex);
+                }
+                continue;
+            }
         }
         // a2: window tops; raise ktop_next of the row's group where needed
         int changed = 0;
@@ -271,24 +579,10 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         }
         const bool fold = since + TILE > Cfg::LIMIT;
         const int any = __syncthreads_or(changed);  // also: previous tile's deposits are done
+        if (!(ONCHIP_FAST && !small_g)) refill();
         if (any || fold) {
             // fold counters into the level sums and demote moved groups
-            if (REGTOT) {
-#pragma unroll
-                for (int j = 0; j < GPT; ++j)
-                    if (tid + j * TPB < G)
-                        fold_group<DT, K>(cnt + (size_t)(tid + j * TPB) * CWP, treg[j], fold, ktop_cur, ktop_next,
-                                          tid + j * TPB);
-            } else {
-                for (int g = tid; g < G; g += TPB) {
-                    int64_t t[K];
-#pragma unroll
-                    for (int l = 0; l < K; ++l) t[l] = tot[(size_t)g * K + l];
-                    fold_group<DT, K>(cnt + (size_t)g * CWP, t, fold, ktop_cur, ktop_next, g);
-#pragma unroll
-                    for (int l = 0; l < K; ++l) tot[(size_t)g * K + l] = t[l];
-                }
-            }
+            fold_all(fold);
             if (any) {  // new block-uniform top?
                 if (tid == 0) { kminmax[0] = 1 << 30; kminmax[1] = -1; }
                 __syncthreads();
@@ -313,34 +607,33 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         if (small_g) {
 #pragma unroll
             for (int i = 0; i < R; ++i)
-                deposit_row<DT, K, true>(cnt, key[i], F::mul(val[i], F::pow2(F::m - F::W * kc[i])), lane);
+                deposit_row<DT, K, true>(cnt, gq, key[i], F::mul(val[i], F::pow2(F::m - F::W * kc[i])), lane);
         } else if (kuni >= 0) {
             const V scale = F::pow2(F::m - F::W * kuni);
 #pragma unroll
-            for (int i = 0; i < R; ++i) deposit_row<DT, K, false>(cnt, key[i], F::mul(val[i], scale), lane);
+            for (int i = 0; i < R; ++i) deposit_row<DT, K, false>(cnt, gq, key[i], F::mul(val[i], scale), lane);
         } else {
 #pragma unroll
             for (int i = 0; i < R; ++i)
-                deposit_row<DT, K, false>(cnt, key[i], F::mul(val[i], F::pow2(F::m - F::W * kc[i])), lane);
+                deposit_row<DT, K, false>(cnt, gq, key[i], F::mul(val[i], F::pow2(F::m - F::W * kc[i])), lane);
         }
     }
 
-    // flush: fold the counters, then publish the block's table
+    // flush: publish the block's table (level sums + unfolded counters)
     __syncthreads();
     auto pub = [&](int g, const int64_t(&t)[K]) {
-        const uint32_t *c = cnt + (size_t)g * CWP;
         if (MODE == 0) {
-            publish_group<DT, K>(c, t, ktop_cur[g], g, out.kglob, out.slots);
+            publish_group<DT, K>(cnt, gq, t, ktop_cur[g], g, out.kglob, out.slots);
         } else {
             out.pk[g] = ktop_cur[g];
 #pragma unroll
-            for (int l = 0; l < K; ++l) out.pT[(size_t)g * K + l] = t[l] + counters_value<DT, K>(c, l);
+            for (int l = 0; l < K; ++l) out.pT[(size_t)g * K + l] = t[l] + counters_value<DT, K>(cnt, gq, g, l);
         }
     };
     if (REGTOT) {
 #pragma unroll
-        for (int j = 0; j < GPT; ++j)
-            if (tid + j * TPB < G) pub(tid + j * TPB, treg[j]);
+        for (int j = 0; j < 4; ++j)
+            if (4 * tid + j < G) pub(4 * tid + j, treg[j]);
     } else {
         for (int g = tid; g < G; g += TPB) {
             int64_t t[K];
@@ -351,6 +644,5 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
     }
     __syncthreads();  // the table may be re-initialised by the caller next
 }
-
 
 }  // namespace repro

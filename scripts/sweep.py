@@ -49,6 +49,7 @@ def main():
     ap.add_argument("--fold", type=int, default=3)
     ap.add_argument("--skew", action="store_true")
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--nobase", action="store_true", help="skip the atomicAdd baseline")
     ap.add_argument("--pm1", action="store_true", help="values U[-1,1) (config 2)")
     a = ap.parse_args()
     dtype = torch.float64 if a.dtype == "f64" else torch.float32
@@ -66,12 +67,12 @@ def main():
         R.timing_enable(False)
         pk = {k: round(v[1], 4) for k, v in R.timing_collect().items()}
         path = R.last_path()
-        tbs = [timeit(lambda: R.baseline_atomic_sum(keys, vals, G, variant=0))]
+        tbs = [] if a.nobase else [timeit(lambda: R.baseline_atomic_sum(keys, vals, G, variant=0))]
         try:
             tbs.append(timeit(lambda: R.baseline_atomic_sum(keys, vals, G, variant=1)))
         except R.ReproError:
             pass
-        tb = min(tbs)
+        tb = min(tbs) if tbs else float("nan")
         gbs = a.n * (4 + vsz) / (t * 1e-3) / 1e9
         print(f"v{a.variant} path{path} G={G:8d} repro {t:.4f} ms ({gbs:7.1f} GB/s, {gbs / 6554.2:.3f} of HBM)  atomic {tb:.4f} ms  "
               f"slowdown {t / tb:.2f}  kernels {pk}", flush=True)
