@@ -25,6 +25,12 @@ namespace repro {
 #ifndef ONCHIP_SKIPZ
 #define ONCHIP_SKIPZ 1
 #endif
+#ifndef ONCHIP_SMALLG
+#define ONCHIP_SMALLG 0  // groups up to which the generic path's warp-uniform REDUX is used
+#endif
+#ifndef ONCHIP_LANEREP
+#define ONCHIP_LANEREP 32  // groups up to which the counters have one copy per lane (<= LANE_G)
+#endif
 #ifndef ONCHIP_NB
 #define ONCHIP_NB 4
 #endif
@@ -47,6 +53,11 @@ struct OnchipCfg {
     static constexpr int LIMBS = Fmt<DT>::LIMBS;
     static constexpr int CW = K * LIMBS;  // 32-bit counters per group
     static constexpr int REG_GQ = 4 * TPB;  // groups covered when level sums are in registers (4 per thread)
+    // small G (<= LANE_G): one counter copy per lane -- counter w of group g
+    // for lane l at cnt[w * REG_GQ + 32 g + l], always bank l -- because 32
+    // lanes adding to a few shared words serialise; level sums in shared
+    // memory per counter word (int64 [LANE_G][CW])
+    static constexpr int LANE_G = REG_GQ / 32;
     static_assert(TILE <= LIMIT, "tile larger than limb headroom");
 };
 
@@ -57,14 +68,15 @@ __host__ __device__ inline int onchip_gq(int G, bool regtot) {
 }
 
 // Shared memory of one block: [level sums int64 [GQ][K] (unless REGTOT)]
-// [counters u32 [CW][GQ]] [ktop_cur [GQ]] [ktop_next [GQ]] [16 words misc],
+// [counters u32 [CW][GQ]] [ktop_cur [GQ]] [ktop_next [GQ]] [16 words misc]
+// [REGTOT: lane-copy level sums int64 [LANE_G][CW]],
 // then, for the TMA-fed kernel, 128 bytes of mbarriers and a ring of STAGES
 // tiles of keys + values.
 template <int DT, int K>
 __host__ __device__ inline size_t onchip_table_bytes(int G, bool regtot = false) {
     using C = OnchipCfg<DT, K>;
     const size_t gq = (size_t)onchip_gq<DT, K>(G, regtot);
-    return gq * ((regtot ? 0 : 8 * K) + 4 * C::CW + 8) + 64;
+    return gq * ((regtot ? 0 : 8 * K) + 4 * C::CW + 8) + 64 + (regtot ? (size_t)8 * C::LANE_G * C::CW : 0);
 }
 template <int DT, int K>
 constexpr size_t onchip_ring_bytes() {
@@ -226,15 +238,15 @@ struct Extractors {
 // counter position is updated for every row of the batch unless the whole warp
 // holds zeros there (one vote per position and batch: small digits and values
 // with few significant bits leave whole counters untouched).  Counter w of
-// group g lives at shared address cbase + 4 g + w * wstride.
+// group g lives at shared address cbase + g * kstride + w * wstride.
 template <int DT, int K, int NB>
-__device__ __forceinline__ void deposit_batch(uint32_t cbase, uint32_t wstride, const int32_t *key,
+__device__ __forceinline__ void deposit_batch(uint32_t cbase, uint32_t kstride, uint32_t wstride, const int32_t *key,
                                               const typename Fmt<DT>::V *val, const Extractors<DT, K> &ex) {
     using Cfg = OnchipCfg<DT, K>;
     uint32_t lo[NB][K], hi[NB][K], a[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        a[i] = cbase + 4u * (uint32_t)key[i];
+        a[i] = cbase + kstride * (uint32_t)key[i];
         if (DT == 1) {
             double r = (double)val[i];
 #pragma unroll
@@ -427,9 +439,52 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
     // rows need no per-group lookup (the common case after the first tiles)
     int kuni = 0;
 
+    // small G: per-lane counter copies (OnchipCfg::LANE_G); their level sums
+    // live in shared memory per counter word, rtot[g][w]
+    const bool lanerep = REGTOT && G <= ONCHIP_LANEREP;
+    int64_t *rtot = reinterpret_cast<int64_t *>(kminmax + 16);
+    if (lanerep)
+        for (int i = tid; i < Cfg::LANE_G * CW; i += TPB) rtot[i] = 0;
+    // the fast path's counter base and per-key stride (bytes)
+    const uint32_t fbase = lanerep ? cbase + 4u * lane : cbase;
+    const uint32_t kstride = lanerep ? 128u : 4u;
+
+    // lane-copy fold: one thread per (counter word, group) pair sums the 32
+    // copies (exact in 32 bits: all copies together hold at most LIMIT rows'
+    // worth of limbs) into rtot -- eight 128-bit loads, chunk order rotated by
+    // lane so a warp's loads spread over all banks -- then moved groups are
+    // demoted (rtot shifts by whole levels; the copies are zero after the fold)
+    auto fold_lanes = [&]() {
+        for (int p = tid; p < CW * G; p += TPB) {
+            const int w = p / G, g = p - w * G;
+            uint4 *c = reinterpret_cast<uint4 *>(cnt + (size_t)w * gq + 32 * g);
+            uint32_t sum = 0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int ch = (i + lane) & 7;
+                const uint4 v = c[ch];
+                sum += v.x + v.y + v.z + v.w;
+                c[ch] = make_uint4(0u, 0u, 0u, 0u);
+            }
+            rtot[g * CW + w] += (int64_t)(int32_t)sum;
+        }
+        __syncthreads();
+        for (int g = tid; g < G; g += TPB) {
+            const int sh = ktop_next[g] - ktop_cur[g];
+            if (sh != 0) {
+                for (int l = K - 1; l >= 0; --l)
+                    for (int b = 0; b < Cfg::LIMBS; ++b)
+                        rtot[g * CW + l * Cfg::LIMBS + b] = l - sh >= 0 ? rtot[g * CW + (l - sh) * Cfg::LIMBS + b] : 0;
+                ktop_cur[g] = ktop_next[g];
+            }
+        }
+    };
+
     // fold all counters into the level sums, demoting moved groups
     auto fold_all = [&](bool fold) {
-        if (REGTOT) {
+        if (lanerep) {
+            fold_lanes();
+        } else if (REGTOT) {
             fold_quad<DT, K>(cnt, gq, tid, treg, fold, ktop_cur, ktop_next);
         } else {
             for (int q = tid; q < nq; q += TPB) {
@@ -447,7 +502,7 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         }
     };
 
-    const bool small_g = G <= 32;
+    const bool small_g = G <= ONCHIP_SMALLG;
     int since = 0;  // rows' worth of digits in the counters since the last fold
 
     // a1: coalesced loads (immediate offsets i*TPB from one base pointer),
@@ -549,8 +604,10 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                 constexpr int NB = ONCHIP_NB < R ? ONCHIP_NB : R;
 #pragma unroll
                 for (int i0 = 0; i0 < R; i0 += NB) {
-                    if (i0 + NB <= R) deposit_batch<DT, K, NB>(cbase, wstride, key + i0, val + i0, ex);
-                    else deposit_batch<DT, K, (R % NB ? R % NB : NB)>(cbase, wstride, key + i0, val + i0, ex);
+                    if (i0 + NB <= R) deposit_batch<DT, K, NB>(fbase, kstride, wstride, key + i0, val + i0, ex);
+                    else
+                        deposit_batch<DT, K, (R % NB ? R % NB : NB)>(fbase, kstride, wstride, key + i0, val + i0,
+                                                                     ex);
                 }
                 continue;
             }
@@ -608,6 +665,11 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
 #pragma unroll
             for (int i = 0; i < R; ++i)
                 deposit_row<DT, K, true>(cnt, gq, key[i], F::mul(val[i], F::pow2(F::m - F::W * kc[i])), lane);
+        } else if (lanerep) {
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                deposit_row<DT, K, false>(cnt + lane, gq, key[i] >= 0 ? 32 * key[i] : -1,
+                                          F::mul(val[i], F::pow2(F::m - F::W * kc[i])), lane);
         } else if (kuni >= 0) {
             const V scale = F::pow2(F::m - F::W * kuni);
 #pragma unroll
@@ -619,8 +681,13 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         }
     }
 
-    // flush: publish the block's table (level sums + unfolded counters)
+    // flush: publish the block's table (level sums + unfolded counters;
+    // replicated counters are folded first)
     __syncthreads();
+    if (lanerep) {
+        fold_lanes();
+        __syncthreads();
+    }
     auto pub = [&](int g, const int64_t(&t)[K]) {
         if (MODE == 0) {
             publish_group<DT, K>(cnt, gq, t, ktop_cur[g], g, out.kglob, out.slots);
@@ -630,7 +697,16 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
             for (int l = 0; l < K; ++l) out.pT[(size_t)g * K + l] = t[l] + counters_value<DT, K>(cnt, gq, g, l);
         }
     };
-    if (REGTOT) {
+    if (lanerep) {
+        for (int g = tid; g < G; g += TPB) {
+            int64_t t[K];
+#pragma unroll
+            for (int l = 0; l < K; ++l)
+                t[l] = Cfg::LIMBS == 2 ? rtot[g * CW + 2 * l] + rtot[g * CW + 2 * l + 1] * (int64_t)(1 << 20)
+                                       : rtot[g * CW + l];
+            pub(g, t);  // the lane copies are all zero after the final fold
+        }
+    } else if (REGTOT) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             if (4 * tid + j < G) pub(4 * tid + j, treg[j]);

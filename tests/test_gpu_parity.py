@@ -1,9 +1,11 @@
 """GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, bit
 for bit (the type is associative, so the north star's bar is bit-exact).
 
-Sizes span several tiles (3072 rows per tile for binary64, 4096 for binary32,
+Sizes span several tiles (1792 rows per tile for binary64, 3840 for binary32,
 one tile per 256 x R rows) and ragged tails; the full BASELINE sizes are
-covered in test_gpu_full_size.py.
+covered in test_gpu_full_size.py.  The `variant` fixture runs the on-chip
+cases under the TMA-fed kernel, the tile-sorted kernel and the register-load
+kernel (unaligned inputs take that path too).
 """
 import itertools
 
@@ -25,9 +27,10 @@ def R():
     return R
 
 
-@pytest.fixture(params=[1, 2], ids=["atomic", "sorted"])
+@pytest.fixture(params=[1, 2, 3], ids=["atomic", "sorted", "regload"])
 def variant(R, request):
-    """Run a test under both on-chip kernels (per-row atomics / tile-sorted runs)."""
+    """Run a test under each on-chip kernel (TMA-fed per-row atomics /
+    tile-sorted runs / per-row atomics with register loads)."""
     R.set_kernel_variant(request.param)
     yield request.param
     R.set_kernel_variant(0)
@@ -104,6 +107,10 @@ CASES = [
     (np.float64, 2, 333, 250001, 90),
     (np.float64, 4, 77, 50000, 200),
     (np.float64, 3, 1, 40000, 30),
+    (np.float64, 3, 2, 77777, 300),       # per-lane counter copies, level shifts
+    (np.float64, 3, 32, 123457, 120),     # largest G with per-lane copies
+    (np.float64, 3, 33, 123457, 120),     # smallest G without
+    (np.float32, 2, 32, 98765, 40),
     (np.float32, 2, 1024, 4096 * 9 + 5, 10),
     (np.float32, 1, 5, 70001, 40),
     (np.float32, 3, 2000, 300007, 30),
