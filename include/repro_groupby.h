@@ -100,6 +100,49 @@ int repro_groupby_sum_host(const int32_t *keys_host, const void *vals_host,
 void repro_release_cache(void);
 
 /* ------------------------------------------------------------------------
+ * Several aggregates of one key column in one pass
+ * ---------------------------------------------------------------------- */
+
+/* Multi-column GroupBy: SUMs of several value columns plus COUNT, grouped by
+ * one key column (the paper reduces every SQL float aggregate to SUM,
+ * PAPER.md:163-174; the aggregation-heavy query shape of its TPC-H Q1
+ * experiment, stood in for by BASELINE config 4).
+ *   cols:  HOST array of ncols DEVICE pointers, each dtype[n].
+ *   proj:  0 -- outs[c][g] = reproducible sum of cols[c] over group g
+ *             (ncols in [1, 8], binary32 or binary64);
+ *          1 -- the config-4 projection (binary64 only, ncols == 4, columns
+ *             qty, price, disc, tax): outs[0] = SUM(qty), outs[1] =
+ *             SUM(price), outs[2] = SUM(price * (1 - disc)), outs[3] =
+ *             SUM(price * (1 - disc) * (1 + tax)), every product and
+ *             difference rounded separately to binary64 (no FMA; DESIGN.md
+ *             reading A-15).
+ *   outs:  HOST array of (proj ? 4 : ncols) DEVICE pointers, dtype[n_groups].
+ *   counts: DEVICE int64[n_groups] (exact row counts per group) or NULL.
+ * Each SUM has the bits repro_groupby_sum would give on that column; rows
+ * with a bad key raise REPRO_EKEY for the whole call.  One fused pass when
+ * n_groups * (outputs + 1) <= 1024 (the aggregates become virtual groups of
+ * one on-chip table), otherwise one pass per output column.  Blocking. */
+int repro_groupby_sum_multi(const int32_t *keys, const void *const *cols,
+                            int32_t ncols, int32_t proj, int64_t n,
+                            int32_t n_groups, int32_t fold, int32_t dtype,
+                            void *const *outs, int64_t *counts);
+
+/* Workspace bytes of repro_groupby_sum_multi_async (0 on invalid shape). */
+size_t repro_groupby_multi_workspace_bytes(int64_t n, int32_t n_groups,
+                                           int32_t ncols, int32_t proj,
+                                           int32_t fold, int32_t dtype);
+
+/* Stream-ordered form with the caller's workspace and device status word
+ * (conventions of repro_groupby_sum_async). */
+int repro_groupby_sum_multi_async(const int32_t *keys, const void *const *cols,
+                                  int32_t ncols, int32_t proj, int64_t n,
+                                  int32_t n_groups, int32_t fold,
+                                  int32_t dtype, void *const *outs,
+                                  int64_t *counts, void *workspace,
+                                  size_t ws_bytes, void *stream,
+                                  int32_t *d_status);
+
+/* ------------------------------------------------------------------------
  * Accumulator handles: n_groups device-resident repro<ScalarT, fold> states
  * (the paper's intermediate aggregates).  A handle is not
  * thread-safe; distinct handles are independent.  All calls are blocking.
@@ -187,7 +230,8 @@ int repro_baseline_atomic_sum(const int32_t *keys, const void *vals, int64_t n,
 /* Number of kernels the last call on this host thread enqueued. */
 int32_t repro_last_launch_count(void);
 /* Path the last GroupBy call on this host thread took: 0 = on-chip tables,
- * 1 = radix-partitioned, -1 = none. */
+ * 1 = radix-partitioned, 2 = fused multi-column on-chip pass, 3 = multi-column
+ * call run one column at a time, -1 = none. */
 int32_t repro_last_path(void);
 /* Largest n_groups the on-chip path handles for (fold, dtype). */
 int32_t repro_onchip_max_groups(int32_t fold, int32_t dtype);

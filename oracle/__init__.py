@@ -215,3 +215,39 @@ def groupby_sum_select(keys: np.ndarray, vals: np.ndarray, n_groups: int, fold: 
                                       state.ctypes.data if with_state else None,
                                       threads or default_threads())
     return (rc, out, state) if with_state else (rc, out)
+
+
+_PRECEDENCE = (EKEY, EDOM, ERANGE)
+
+
+def q1_project(price: np.ndarray, disc: np.ndarray, tax: np.ndarray):
+    """Config-4 row projection, reading A-15: disc_price =
+    price (x) (1 (-) disc), charge = disc_price (x) (1 (+) tax), each
+    operation one binary64 rounding (numpy elementwise ops, no contraction)."""
+    one = np.float64(1.0)
+    disc_price = np.multiply(price, np.subtract(one, disc))
+    charge = np.multiply(disc_price, np.add(one, tax))
+    return disc_price, charge
+
+
+def groupby_sum_multi(keys: np.ndarray, cols, n_groups: int, fold: int, proj: int = 0, *,
+                      threads: int | None = None):
+    """Several GroupBy-SUMs of one key column plus COUNT (the C-ABI's
+    repro_groupby_sum_multi): each output column is O5 on its value column
+    (proj 1: on the projected columns of q1_project); COUNT is the number of
+    rows per group.  Status: the highest-precedence error of any column
+    (EKEY > EDOM > ERANGE, SPEC.md:211).  Returns (status, [outs], counts)."""
+    keys = np.ascontiguousarray(keys, dtype=np.int32)
+    if proj == 1:
+        qty, price, disc, tax = cols
+        dp, ch = q1_project(price, disc, tax)
+        cols = [qty, price, dp, ch]
+    outs, codes = [], []
+    for c in cols:
+        rc, o = groupby_sum(keys, np.ascontiguousarray(c), n_groups, fold, threads=threads)
+        outs.append(o)
+        codes.append(rc)
+    status = next((e for e in _PRECEDENCE if e in codes), OK)
+    ok = (keys >= 0) & (keys < n_groups)
+    counts = np.bincount(keys[ok], minlength=n_groups).astype(np.int64)
+    return status, outs, counts

@@ -8,6 +8,7 @@ fallback: importing the package fails loudly when the library is missing.
 
 Entry points mirror the C names:
   groupby_sum / groupby_sum_async / groupby_sum_host / workspace_bytes
+  groupby_sum_multi / groupby_sum_multi_async / multi_workspace_bytes
   Accumulator (repro_acc_*), baseline_atomic_sum, and introspection helpers.
 """
 from __future__ import annotations
@@ -46,6 +47,11 @@ _sig("repro_groupby_workspace_bytes", _sz, _i64, _i32, _i32, _i32)
 _sig("repro_groupby_sum_async", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp)
 _sig("repro_groupby_sum_host", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp)
 _sig("repro_release_cache", None)
+_sig("repro_groupby_sum_multi", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
+     ctypes.POINTER(_vp), _vp)
+_sig("repro_groupby_multi_workspace_bytes", _sz, _i64, _i32, _i32, _i32, _i32, _i32)
+_sig("repro_groupby_sum_multi_async", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
+     ctypes.POINTER(_vp), _vp, _vp, _sz, _vp, _vp)
 _sig("repro_acc_create", ctypes.c_int, ctypes.POINTER(_vp), _i32, _i32, _i32)
 _sig("repro_acc_deposit", ctypes.c_int, _vp, _vp, _vp, _i64)
 _sig("repro_acc_merge", ctypes.c_int, _vp, _vp)
@@ -180,6 +186,63 @@ def groupby_sum_host(keys, vals, n_groups: int, fold: int = 3, out=None):
                                      dt, out.data_ptr())
     _check(st, "repro_groupby_sum_host")
     return out
+
+
+def _multi_args(keys, cols, n_groups, proj, outs, counts):
+    torch = _torch()
+    if not cols:
+        raise ValueError("at least one value column")
+    dt = _dtype_code(cols[0])
+    n = keys.numel()
+    for c in cols:
+        if c.dtype != cols[0].dtype or c.numel() != n:
+            raise ValueError("value columns must share dtype and length with keys")
+    nout = 4 if proj == 1 else len(cols)
+    if outs is None:
+        outs = [torch.empty(n_groups, dtype=cols[0].dtype, device=cols[0].device) for _ in range(nout)]
+    cptr = (_vp * len(cols))(*[_dev(c, "cols") for c in cols])
+    optr = (_vp * len(outs))(*[_dev(o, "outs", cols[0].dtype) for o in outs])
+    cnt = _dev(counts, "counts", torch.int64) if counts is not None else None
+    return dt, n, outs, cptr, optr, cnt
+
+
+def groupby_sum_multi(keys, cols, n_groups: int, fold: int = 3, proj: int = 0, outs=None, counts=None,
+                      with_counts: bool = True):
+    """Several reproducible SUMs (+ COUNT) of one key column in one pass
+    (repro_groupby_sum_multi).  proj=1: the config-4 projection over
+    (qty, price, disc, tax).  Returns (list of SUM columns, int64 counts or None)."""
+    torch = _torch()
+    if with_counts and counts is None:
+        counts = torch.empty(n_groups, dtype=torch.int64, device=keys.device)
+    dt, n, outs, cptr, optr, cnt = _multi_args(keys, cols, n_groups, proj, outs, counts if with_counts else None)
+    st = _lib.repro_groupby_sum_multi(_dev(keys, "keys", torch.int32), cptr, len(cols), proj, n, n_groups, fold, dt,
+                                      optr, cnt)
+    _check(st, "repro_groupby_sum_multi")
+    return outs, (counts if with_counts else None)
+
+
+def multi_workspace_bytes(n: int, n_groups: int, ncols: int, proj: int, fold: int, dtype: int) -> int:
+    return _lib.repro_groupby_multi_workspace_bytes(n, n_groups, ncols, proj, fold, dtype)
+
+
+def make_multi_workspace(n, n_groups, ncols, proj, fold, dtype, device="cuda"):
+    torch = _torch()
+    nbytes = multi_workspace_bytes(n, n_groups, ncols, proj, fold, dtype)
+    if nbytes == 0:
+        raise ReproError(EINVAL, "repro_groupby_multi_workspace_bytes")
+    return torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+
+
+def groupby_sum_multi_async(keys, cols, n_groups: int, fold: int, proj: int, outs, counts, workspace, status,
+                            stream=None):
+    torch = _torch()
+    dt, n, outs, cptr, optr, cnt = _multi_args(keys, cols, n_groups, proj, outs, counts)
+    wp, wb = _aligned_ptr(workspace)
+    st = _lib.repro_groupby_sum_multi_async(_dev(keys, "keys", torch.int32), cptr, len(cols), proj, n, n_groups,
+                                            fold, dt, optr, cnt, wp, wb, _stream_ptr(stream),
+                                            _dev(status, "status", torch.int32))
+    _check(st, "repro_groupby_sum_multi_async")
+    return outs
 
 
 def baseline_atomic_sum(keys, vals, n_groups: int, variant: int = 0, accumulate_f64: bool = False, out=None,

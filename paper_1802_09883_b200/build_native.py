@@ -37,23 +37,42 @@ def stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
-    """Compile the library (to `out`, default LIB) with optional -D defines."""
+    """Compile the library (to `out`, default LIB) with optional -D defines:
+    every .cu to an object in parallel, then one shared-library link."""
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
+
     target = out or LIB
     if not force and out is None and not stale():
         return LIB
     os.makedirs(os.path.dirname(target), exist_ok=True)
-    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-shared", "-I", os.path.join(ROOT, "include"),
-           "-I", CSRC, *sources(), "-o", target + ".tmp"]
-    res = subprocess.run(cmd, capture_output=True, text=True)
+    common = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    tmp = tempfile.mkdtemp(prefix="repro_build_")
+    srcs = sources()
+    objs = [os.path.join(tmp, os.path.basename(s) + ".o") for s in srcs]
+
+    def compile_one(i):
+        return subprocess.run(common + ["-c", srcs[i], "-o", objs[i]], capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(compile_one, range(len(srcs))))
+    link = subprocess.run([NVCC, *ARCH, "-shared", *objs, "-o", target + ".tmp"], capture_output=True, text=True)
     log = os.path.join(LIBDIR, "build.log") if out is None else target + ".log"
     with open(log, "w") as fh:
-        fh.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        sys.stderr.write(res.stdout + res.stderr)
+        for s_, r in zip(srcs, results):
+            fh.write(" ".join(common + ["-c", s_]) + "\n" + r.stdout + r.stderr)
+        fh.write(link.stdout + link.stderr)
+    failed = [r for r in results if r.returncode != 0] + ([link] if link.returncode != 0 else [])
+    for o in objs:
+        if os.path.exists(o):
+            os.remove(o)
+    os.rmdir(tmp)
+    if failed:
+        sys.stderr.write("".join(r.stdout + r.stderr for r in failed))
         raise RuntimeError("nvcc failed building librepro_b200.so")
     os.replace(target + ".tmp", target)
     if verbose:
-        print(res.stderr)
+        print("".join(r.stderr for r in results))
     return target
 
 

@@ -335,6 +335,165 @@ int repro_groupby_sum(const int32_t *keys, const void *vals, int64_t n, int32_t 
     return finish_blocking(flags, 0);
 }
 
+// ---- multi-column GroupBy (several SUMs + COUNT in one pass) ---------------
+
+}  // extern "C"
+
+namespace {
+
+int multi_nout(int32_t proj, int32_t ncols) { return proj == 1 ? 4 : ncols; }
+
+bool multi_valid(int64_t n, int32_t G, int32_t ncols, int32_t proj, int32_t K, int32_t dt) {
+    if (n < 0 || !valid_shape(G, K, dt)) return false;
+    if (proj == 1) return ncols == 4 && dt == REPRO_F64;
+    return proj == 0 && ncols >= 1 && ncols <= 8;
+}
+
+// fused on-chip kernel applies: virtual groups G * NV fit the register tables
+bool multi_fused(int32_t G, int32_t ncols, int32_t proj) {
+    const int nv = multi_virtual_columns(proj, ncols);
+    return nv > 0 && (int64_t)G * nv <= 1024;
+}
+
+// fused workspace: [on-chip zeroed region for G*NV groups | virtual results]
+// fallback workspace: [flags accumulator | 2 projected columns (proj 1) |
+// one single-column workspace, reused column after column]
+size_t multi_ws_bytes(int64_t n, int32_t G, int32_t ncols, int32_t proj, int32_t K, int32_t dt) {
+    const size_t vsz = dt == REPRO_F64 ? 8 : 4;
+    if (multi_fused(G, ncols, proj)) {
+        const int32_t Gv = G * multi_virtual_columns(proj, ncols);
+        return onchip_ws_bytes(n, Gv, K, dt) + align_up(vsz * (size_t)Gv);
+    }
+    const int path = choose_path(G, K, dt);
+    if (path < 0) return 0;
+    return ALIGN + (proj == 1 ? 2 * align_up(8 * (size_t)n) : 0) + ws_bytes_for(path, n, G, K, dt);
+}
+
+int enqueue_multi(const int32_t *keys, const void *const *cols, int32_t ncols, int32_t proj, int64_t n, int32_t G,
+                  int32_t K, int32_t dt, void *const *outs, int64_t *counts, void *ws, size_t ws_bytes,
+                  cudaStream_t st, uint32_t **flags_out) {
+    if (ws_bytes < multi_ws_bytes(n, G, ncols, proj, K, dt)) return REPRO_ENOMEM;
+    const int nout = multi_nout(proj, ncols);
+    if (multi_fused(G, ncols, proj)) {
+        const int nv = multi_virtual_columns(proj, ncols);
+        const int32_t Gv = G * nv;
+        t_path = 2;
+        OnchipWs w = carve_onchip(ws, n, Gv, K, dt);
+        void *vout = (char *)ws + onchip_ws_bytes(n, Gv, K, dt);
+        *flags_out = w.flags;
+        if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
+        int rc = timed("onchip_accumulate", st, [&] {
+            return launch_onchip_multi(dt, K, proj, ncols, keys, cols, n, G, w.kglob, w.slots, w.flags, st,
+                                       &t_launches);
+        });
+        if (rc) return map_launch(rc);
+        rc = timed("fold", st, [&] {
+            return launch_fold(dt, K, Gv, w.kglob, w.slots, 0, nullptr, nullptr, nullptr, vout, w.flags, st,
+                               &t_launches);
+        });
+        if (rc) return map_launch(rc);
+        rc = timed("scatter", st, [&] {
+            return launch_multi_scatter(dt, K, vout, G, nout, outs, w.slots, counts, st, &t_launches);
+        });
+        return map_launch(rc);
+    }
+    // fallback: one GroupBy pass per output column (projection materialised),
+    // COUNT by integer atomics; status bits OR-ed over the passes
+    t_path = 3;
+    char *p = (char *)ws;
+    uint32_t *acc = (uint32_t *)p;
+    p += ALIGN;
+    *flags_out = acc;
+    if (cudaMemsetAsync(acc, 0, ALIGN, st) != cudaSuccess) return REPRO_ECUDA;
+    const void *src[4] = {nullptr, nullptr, nullptr, nullptr};
+    if (proj == 1) {
+        double *dp = (double *)p, *charge = (double *)(p + align_up(8 * (size_t)n));
+        p += 2 * align_up(8 * (size_t)n);
+        int rc = timed("project", st, [&] {
+            return launch_q1_project((const double *)cols[1], (const double *)cols[2], (const double *)cols[3], n,
+                                     dp, charge, st, &t_launches);
+        });
+        if (rc) return map_launch(rc);
+        src[0] = cols[0];
+        src[1] = cols[1];
+        src[2] = dp;
+        src[3] = charge;
+    }
+    const size_t rest = ws_bytes - (size_t)(p - (char *)ws);
+    for (int c = 0; c < nout; ++c) {
+        uint32_t *f = nullptr;
+        int rc = enqueue_groupby(keys, proj == 1 ? src[c] : cols[c], n, G, K, dt, outs[c], 0, nullptr, nullptr,
+                                 nullptr, p, rest, st, &f);
+        if (rc != REPRO_OK) return rc;
+        rc = launch_flags_or(acc, f, st, &t_launches);
+        if (rc) return map_launch(rc);
+    }
+    if (counts) {
+        int rc = timed("count", st, [&] { return launch_count_rows(keys, n, G, counts, st, &t_launches); });
+        if (rc) return map_launch(rc);
+    }
+    t_path = 3;
+    return REPRO_OK;
+}
+
+bool multi_ptrs_ok(int64_t n, const int32_t *keys, const void *const *cols, int32_t ncols, void *const *outs,
+                   int nout) {
+    if (!cols || !outs) return false;
+    for (int c = 0; c < nout; ++c)
+        if (!outs[c]) return false;
+    if (n > 0) {
+        if (!keys) return false;
+        for (int c = 0; c < ncols; ++c)
+            if (!cols[c]) return false;
+    }
+    return true;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t repro_groupby_multi_workspace_bytes(int64_t n, int32_t n_groups, int32_t ncols, int32_t proj, int32_t fold,
+                                           int32_t dtype) {
+    if (!multi_valid(n, n_groups, ncols, proj, fold, dtype)) return 0;
+    return multi_ws_bytes(n, n_groups, ncols, proj, fold, dtype);
+}
+
+int repro_groupby_sum_multi_async(const int32_t *keys, const void *const *cols, int32_t ncols, int32_t proj,
+                                  int64_t n, int32_t n_groups, int32_t fold, int32_t dtype, void *const *outs,
+                                  int64_t *counts, void *workspace, size_t ws_bytes, void *stream,
+                                  int32_t *d_status) {
+    t_launches = 0;
+    if (!multi_valid(n, n_groups, ncols, proj, fold, dtype) || !workspace || !d_status) return REPRO_EINVAL;
+    if (!multi_ptrs_ok(n, keys, cols, ncols, outs, multi_nout(proj, ncols))) return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *flags = nullptr;
+    int rc = enqueue_multi(keys, cols, ncols, proj, n, n_groups, fold, dtype, outs, counts, workspace, ws_bytes, st,
+                           &flags);
+    if (rc != REPRO_OK) return rc;
+    return map_launch(timed("status", st, [&] { return launch_status(flags, d_status, st, &t_launches); }));
+}
+
+int repro_groupby_sum_multi(const int32_t *keys, const void *const *cols, int32_t ncols, int32_t proj, int64_t n,
+                            int32_t n_groups, int32_t fold, int32_t dtype, void *const *outs, int64_t *counts) {
+    t_launches = 0;
+    if (!multi_valid(n, n_groups, ncols, proj, fold, dtype)) return REPRO_EINVAL;
+    if (!multi_ptrs_ok(n, keys, cols, ncols, outs, multi_nout(proj, ncols))) return REPRO_EINVAL;
+    const size_t need = multi_ws_bytes(n, n_groups, ncols, proj, fold, dtype);
+    if (need == 0) return REPRO_EINVAL;
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    void *ws = cache_get(need);
+    if (!ws) return REPRO_ENOMEM;
+    uint32_t *flags = nullptr;
+    int rc = enqueue_multi(keys, cols, ncols, proj, n, n_groups, fold, dtype, outs, counts, ws, need, 0, &flags);
+    if (rc != REPRO_OK) {
+        cudaStreamSynchronize(0);
+        return rc;
+    }
+    return finish_blocking(flags, 0);
+}
+
 void repro_release_cache(void) {
     std::lock_guard<std::mutex> lock(g_cache.mu);
     if (g_cache.ptr) cudaFree(g_cache.ptr);

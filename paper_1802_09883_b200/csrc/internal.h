@@ -34,6 +34,21 @@ int launch_onchip_any(int DT, int K, const int32_t *keys, const void *vals, int6
                       int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
                       int *launches);
 
+// multi-column on-chip GroupBy (k_onchip.cu): virtual columns per group for a
+// (proj, ncols) shape (-1: no fused kernel), and the launcher over G real
+// groups (virtual groups j * G + g; -1 if this shape cannot run fused)
+int multi_virtual_columns(int proj, int ncols);
+int launch_onchip_multi(int DT, int K, int proj, int ncols, const int32_t *keys, const void *const *cols, int64_t n,
+                        int32_t G, int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
+                        int *launches);
+
+int launch_multi_scatter(int DT, int K, const void *vout, int32_t G, int nsum, void *const *outs,
+                         const unsigned long long *slots, int64_t *counts, cudaStream_t st, int *launches);
+int launch_q1_project(const double *price, const double *disc, const double *tax, int64_t n, double *dp,
+                      double *charge, cudaStream_t st, int *launches);
+int launch_count_rows(const int32_t *keys, int64_t n, int32_t G, int64_t *counts, cudaStream_t st, int *launches);
+int launch_flags_or(uint32_t *acc, const uint32_t *f, cudaStream_t st, int *launches);
+
 // slots (+ global tops) -> canonical state; optionally merged with the
 // existing state (acc_*), optionally finalised into out.  `merge` != 0 reads
 // acc_k/acc_C/acc_D as the previous state.

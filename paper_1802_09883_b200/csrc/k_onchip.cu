@@ -27,68 +27,19 @@
 #include "common.cuh"
 #include "internal.h"
 #include "onchip_core.cuh"
+#include "onchip_launch.cuh"
 
 #include <algorithm>
 #include <cstdlib>
 
-#ifndef ONCHIP_TMA
-#define ONCHIP_TMA 1
-#endif
 
 namespace repro {
-
-static int onchip_variant();
-
-template <int DT, int K, bool REGTOT, bool TMA>
-__global__ void __launch_bounds__(256, ONCHIP_MINBLOCKS)
-k_onchip_accumulate(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals,
-                    int64_t n, int32_t G, int64_t chunk, int32_t *__restrict__ kglob,
-                    unsigned long long *__restrict__ slots, uint32_t *__restrict__ status) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int64_t row0 = (int64_t)blockIdx.x * chunk;
-    const int64_t row1 = min(n, row0 + chunk);
-    uint32_t flags = 0;
-    PubArgs out{kglob, slots, nullptr, nullptr};
-    accumulate_range<DT, K, REGTOT, 0, TMA>(keys, vals, row0, row1, G, smem, flags, out);
-    flags = __reduce_or_sync(0xffffffffu, flags);
-    if ((threadIdx.x & 31) == 0 && flags) atomicOr(status, flags);
-}
 
 template <int DT, int K>
 int launch_onchip(const int32_t *keys, const void *vals, int64_t n, int32_t G, int32_t *kglob,
                   unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches) {
-    using Cfg = OnchipCfg<DT, K>;
-    const bool regtot = G <= Cfg::REG_GQ;  // level sums in registers
-    // TMA-fed ring when both columns are 16-byte aligned and the ring fits
-    const size_t table = onchip_smem_bytes<DT, K>(G, regtot);
-    const bool tma = ONCHIP_TMA && onchip_variant() != 3 && ((((uintptr_t)keys) | ((uintptr_t)vals)) & 15) == 0 &&
-                     table + onchip_ring_bytes<DT, K>() <= (size_t)device_props().smem_optin;
-    auto kern = regtot ? (tma ? k_onchip_accumulate<DT, K, true, true> : k_onchip_accumulate<DT, K, true, false>)
-                       : (tma ? k_onchip_accumulate<DT, K, false, true> : k_onchip_accumulate<DT, K, false, false>);
-    const size_t smem = table + (tma ? onchip_ring_bytes<DT, K>() : 0);
-    if (smem > (size_t)device_props().smem_optin) return -1;
-    static thread_local int configured_smem[2][5][2][2] = {};
-    if (configured_smem[DT][K][regtot][tma] < (int)smem) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-            return -2;
-        configured_smem[DT][K][regtot][tma] = (int)smem;
-    }
-    if (n == 0) return 0;
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Cfg::TPB, smem);
-    if (per_sm < 1) return -1;
-    int64_t grid = (int64_t)per_sm * device_props().sms;
-    // a block's int64 level sums must not overflow: <= 2^23 rows per block
-    const int64_t min_grid = (n + (1ll << 23) - 1) >> 23;
-    if (grid < min_grid) grid = min_grid;
-    int64_t chunk = (n + grid - 1) / grid;
-    chunk = ((chunk + Cfg::TILE - 1) / Cfg::TILE) * Cfg::TILE;
-    if (chunk > (1ll << 23)) chunk = 1ll << 23;
-    grid = (n + chunk - 1) / chunk;
-    kern<<<(unsigned)grid, Cfg::TPB, smem, st>>>(keys, (const typename Fmt<DT>::V *)vals, n, G, chunk,
-                                                 kglob, slots, status);
-    ++*launches;
-    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+    const SrcSingle<DT> src{{(const typename Fmt<DT>::V *)vals}, G};
+    return launch_onchip_src<DT, K, SrcSingle<DT>, true>(keys, src, n, G, kglob, slots, status, st, launches);
 }
 
 int atomic_max_groups(int K, int DT) {
@@ -104,7 +55,7 @@ int atomic_max_groups(int K, int DT) {
 // 2 = sorted, 3 = atomic with register loads only.
 // Initialised from REPRO_ONCHIP_VARIANT, settable through the C-ABI.
 static int g_variant = -1;
-static int onchip_variant() {
+int onchip_variant() {
     if (g_variant < 0) {
         const char *e = getenv("REPRO_ONCHIP_VARIANT");
         g_variant = (e && e[0] == 'a') ? 1 : (e && e[0] == 's') ? 2 : (e && e[0] == 'r') ? 3 : 0;

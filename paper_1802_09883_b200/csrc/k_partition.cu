@@ -327,7 +327,8 @@ k_part_accumulate(const int32_t *__restrict__ pkeys, const typename Fmt<DT>::V *
         const int p = iown[it];
         const int Gi = min(PART_GP, G - p * PART_GP);
         PubArgs out{nullptr, nullptr, pk + (size_t)it * PART_GP, pT + (size_t)it * PART_GP * K};
-        accumulate_range<DT, K, true, 1>(pkeys, pvals, items[2 * it], items[2 * it + 1], Gi, smem, flags, out);
+        const SrcSingle<DT> src{{pvals}, Gi};
+        accumulate_range<DT, K, true, 1>(pkeys, src, items[2 * it], items[2 * it + 1], Gi, smem, flags, out);
     }
     flags = __reduce_or_sync(0xffffffffu, flags);
     if ((threadIdx.x & 31) == 0 && flags) atomicOr(status, flags);

@@ -31,6 +31,9 @@ namespace repro {
 #ifndef ONCHIP_LANEREP
 #define ONCHIP_LANEREP 32  // groups up to which the counters have one copy per lane (<= LANE_G)
 #endif
+#ifndef ONCHIP_RMULTI
+#define ONCHIP_RMULTI 2  // input rows per thread per tile of the multi-column sources
+#endif
 #ifndef ONCHIP_NB
 #define ONCHIP_NB 4
 #endif
@@ -78,10 +81,10 @@ __host__ __device__ inline size_t onchip_table_bytes(int G, bool regtot = false)
     const size_t gq = (size_t)onchip_gq<DT, K>(G, regtot);
     return gq * ((regtot ? 0 : 8 * K) + 4 * C::CW + 8) + 64 + (regtot ? (size_t)8 * C::LANE_G * C::CW : 0);
 }
-template <int DT, int K>
+template <int DT, int K, int NCOL = 1, int RIN = OnchipCfg<DT, K>::R>
 constexpr size_t onchip_ring_bytes() {
     using C = OnchipCfg<DT, K>;
-    return 128 + (size_t)ONCHIP_STAGES * C::TILE * (4 + sizeof(typename Fmt<DT>::V));
+    return 128 + (size_t)ONCHIP_STAGES * C::TPB * RIN * (4 + NCOL * sizeof(typename Fmt<DT>::V));
 }
 template <int DT, int K>
 size_t onchip_smem_bytes(int G, bool regtot = false, bool tma = false) {
@@ -390,6 +393,71 @@ __device__ __forceinline__ int check_row(int key, typename Fmt<DT>::V v, bool in
     return (in && bad == 0u) ? key : -1;
 }
 
+// ---- row sources -----------------------------------------------------------
+// accumulate_range reads, per input row, one int32 key and NCOL value columns
+// and turns them into NV virtual rows (virtual key, value); every virtual row
+// is deposited like a row of a single-column GroupBy over the virtual groups.
+// R = input rows per thread per tile.
+
+// plain GroupBy-SUM of one column
+template <int DT>
+struct SrcSingle {
+    using V = typename Fmt<DT>::V;
+    static constexpr int NCOL = 1, NV = 1;
+    static constexpr int R = (DT == 1) ? ONCHIP_R64 : ONCHIP_R32;
+    const V *col[NCOL];
+    int G;
+    __device__ __forceinline__ void expand(int32_t key, const V (&c)[NCOL], int32_t (&vk)[NV], V (&vv)[NV]) const {
+        vk[0] = key;
+        vv[0] = c[0];
+    }
+};
+
+// NC columns summed independently plus COUNT: virtual group j * G + g for
+// column j, and column NC holds the value 1 for every row (a reproducible sum
+// of ones is the exact row count).  Rows with a key outside [0, G) map to
+// virtual key -1 (flagged EKEY, never deposited).
+template <int DT, int NC>
+struct SrcCols {
+    using V = typename Fmt<DT>::V;
+    static constexpr int NCOL = NC, NV = NC + 1;
+    static constexpr int R = ONCHIP_RMULTI;
+    const V *col[NCOL];
+    int G;
+    __device__ __forceinline__ void expand(int32_t key, const V (&c)[NCOL], int32_t (&vk)[NV], V (&vv)[NV]) const {
+        const bool ok = (uint32_t)key < (uint32_t)G;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            vk[j] = ok ? key + j * G : -1;
+            vv[j] = j < NC ? c[j < NC ? j : 0] : V(1);
+        }
+    }
+};
+
+// The aggregation-heavy query shape of BASELINE config 4 (reading A-15):
+// columns (qty, price, disc, tax) -> SUMs of qty, price, disc_price =
+// price (x) (1 (-) disc), charge = disc_price (x) (1 (+) tax), each operation
+// rounded once (no contraction), plus COUNT.
+struct SrcQ1 {
+    using V = double;
+    static constexpr int NCOL = 4, NV = 5;
+    static constexpr int R = ONCHIP_RMULTI;
+    const double *col[NCOL];
+    int G;
+    __device__ __forceinline__ void expand(int32_t key, const double (&c)[NCOL], int32_t (&vk)[NV],
+                                           double (&vv)[NV]) const {
+        const bool ok = (uint32_t)key < (uint32_t)G;
+        const double dp = __dmul_rn(c[1], __dsub_rn(1.0, c[2]));
+        vv[0] = c[0];
+        vv[1] = c[1];
+        vv[2] = dp;
+        vv[3] = __dmul_rn(dp, __dadd_rn(1.0, c[3]));
+        vv[4] = 1.0;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) vk[j] = ok ? key + j * G : -1;
+    }
+};
+
 // Where a block's finished table goes: MODE 0 adds it into the absolute-level
 // slot table (kglob, slots); MODE 1 writes it densely as one partial state per
 // group (pk[g], pT[g*K + l]) for the partitioned path's merge.
@@ -403,15 +471,22 @@ struct PubArgs {
 // One block deposits rows [row0, row1) of (keys, vals) into a fresh table of G
 // groups in shared memory (+ registers) and publishes it.  Must be entered by
 // all threads of the block; `smem` is the dynamic shared memory.
-template <int DT, int K, bool REGTOT, int MODE, bool TMA = false>
-__device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ keys,
-                                                 const typename Fmt<DT>::V *__restrict__ vals, int64_t row0,
+//
+// G is the number of (virtual) groups of the table; SRC (row sources above)
+// says how input rows become virtual rows.
+template <int DT, int K, bool REGTOT, int MODE, bool TMA = false, class SRC = SrcSingle<DT>>
+__device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ keys, const SRC &src, int64_t row0,
                                                  int64_t row1, int32_t G, unsigned char *smem, uint32_t &flags,
                                                  const PubArgs &out) {
     using F = Fmt<DT>;
     using V = typename F::V;
     using Cfg = OnchipCfg<DT, K>;
-    constexpr int TPB = Cfg::TPB, R = Cfg::R, TILE = Cfg::TILE, CW = Cfg::CW;
+    constexpr int NCOL = SRC::NCOL, NV = SRC::NV;
+    constexpr int TPB = Cfg::TPB, RIN = SRC::R, TILE = TPB * RIN, CW = Cfg::CW;
+    constexpr int R = RIN * NV;            // virtual rows per thread per tile
+    constexpr int VTILE = TILE * NV;       // virtual rows per tile (fold accounting)
+    constexpr size_t ROWB = 4 + NCOL * sizeof(V);  // bytes per input row in a ring stage
+    static_assert(VTILE <= Cfg::LIMIT, "tile larger than limb headroom");
     const int gq = onchip_gq<DT, K>(G, REGTOT);
     const int nq = gq >> 2;  // group quads
 
@@ -507,15 +582,26 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
 
     // a1: coalesced loads (immediate offsets i*TPB from one base pointer),
     // bounds-checked, straight from global memory
-    auto load_tile = [&](int64_t b, int32_t(&k)[R], V(&v)[R]) {
-        const int32_t *kp = keys + b + tid;
-        const V *vp = vals + b + tid;
+    auto expand_row = [&](int i, bool in, int32_t k, const V (&c)[NCOL], int32_t(&key)[R], V(&val)[R]) {
+        int32_t vk[NV];
+        V vv[NV];
+        src.expand(k, c, vk, vv);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            key[i * NV + j] = in ? vk[j] : -1;
+            val[i * NV + j] = in ? vv[j] : V(0);
+        }
+    };
+    auto load_tile = [&](int64_t b, int32_t(&key)[R], V(&val)[R]) {
         const int rm = (int)min((int64_t)TILE, row1 - b) - tid;
 #pragma unroll
-        for (int i = 0; i < R; ++i) {
+        for (int i = 0; i < RIN; ++i) {
             const bool in = i * TPB < rm;
-            k[i] = in ? __ldg(kp + i * TPB) : -1;
-            v[i] = in ? __ldg(vp + i * TPB) : V(0);
+            const int64_t r = b + tid + i * TPB;
+            V c[NCOL];
+#pragma unroll
+            for (int j = 0; j < NCOL; ++j) c[j] = in ? __ldg(src.col[j] + r) : V(0);
+            expand_row(i, in, in ? __ldg(keys + r) : -1, c, key, val);
         }
     };
     // TMA-fed variant: full tiles stream through a ring of STAGES shared
@@ -528,12 +614,15 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
     constexpr int S = ONCHIP_STAGES;
     const size_t tbytes = (onchip_table_bytes<DT, K>(G, REGTOT) + 127) & ~(size_t)127;
     const uint32_t ring = (uint32_t)__cvta_generic_to_shared(smem) + (uint32_t)tbytes;  // mbarriers, then tiles
-    auto stage_keys = [&](int st) { return ring + 128u + (uint32_t)st * (uint32_t)(TILE * (4 + sizeof(V))); };
+    auto stage_keys = [&](int st) { return ring + 128u + (uint32_t)st * (uint32_t)(TILE * ROWB); };
     auto issue = [&](int64_t t_base, int st) {  // thread 0 only; full tiles only
         const uint32_t bar = ring + 8u * st;
-        mbar_expect_tx(bar, (uint32_t)(TILE * (4 + sizeof(V))));
+        mbar_expect_tx(bar, (uint32_t)(TILE * ROWB));
         tma_load_1d(stage_keys(st), keys + t_base, TILE * 4, bar);
-        tma_load_1d(stage_keys(st) + TILE * 4, vals + t_base, TILE * sizeof(V), bar);
+#pragma unroll
+        for (int j = 0; j < NCOL; ++j)
+            tma_load_1d(stage_keys(st) + (uint32_t)(TILE * (4 + j * sizeof(V))), src.col[j] + t_base,
+                        TILE * sizeof(V), bar);
     };
     if (TMA) {
         if (tid == 0) {
@@ -555,11 +644,15 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         if (TMA && base + TILE <= row1) {
             const int st = tile % S;
             mbar_wait(ring + 8u * st, (uint32_t)((tile / S) & 1));
-            const int32_t *sk =
-                reinterpret_cast<const int32_t *>(smem + tbytes + 128 + (size_t)st * TILE * (4 + sizeof(V)));
+            const int32_t *sk = reinterpret_cast<const int32_t *>(smem + tbytes + 128 + (size_t)st * TILE * ROWB);
             const V *sv = reinterpret_cast<const V *>(sk + TILE);
 #pragma unroll
-            for (int i = 0; i < R; ++i) { key[i] = sk[tid + i * TPB]; val[i] = sv[tid + i * TPB]; }
+            for (int i = 0; i < RIN; ++i) {
+                V c[NCOL];
+#pragma unroll
+                for (int j = 0; j < NCOL; ++j) c[j] = sv[j * TILE + tid + i * TPB];
+                expand_row(i, true, sk[tid + i * TPB], c, key, val);
+            }
         } else {
             load_tile(base, key, val);
         }
@@ -594,12 +687,12 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
             const int any_slow = __syncthreads_or(slow);
             refill();
             if (!any_slow) {
-                if (since + TILE > Cfg::LIMIT) {
+                if (since + VTILE > Cfg::LIMIT) {
                     fold_all(true);
                     since = 0;
                     __syncthreads();
                 }
-                since += TILE;
+                since += VTILE;
                 const Extractors<DT, K> ex(kuni);
                 constexpr int NB = ONCHIP_NB < R ? ONCHIP_NB : R;
 #pragma unroll
@@ -618,7 +711,7 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 int ks;
-                const int k = check_row<DT>(key[i], val[i], i * TPB < rem, G, flags, ks);
+                const int k = check_row<DT>(key[i], val[i], (i / NV) * TPB < rem, G, flags, ks);
                 if (k >= 0 && ks > kuni) { atomicMax(&ktop_next[k], ks); changed = 1; }
                 key[i] = k;
                 kc[i] = kuni;
@@ -627,14 +720,14 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 int ks;
-                const int k = check_row<DT>(key[i], val[i], i * TPB < rem, G, flags, ks);
+                const int k = check_row<DT>(key[i], val[i], (i / NV) * TPB < rem, G, flags, ks);
                 const int cur = k >= 0 ? ktop_cur[k] : 0;
                 if (k >= 0 && ks > cur) { atomicMax(&ktop_next[k], ks); changed = 1; }
                 key[i] = k;
                 kc[i] = cur;
             }
         }
-        const bool fold = since + TILE > Cfg::LIMIT;
+        const bool fold = since + VTILE > Cfg::LIMIT;
         const int any = __syncthreads_or(changed);  // also: previous tile's deposits are done
         if (!(ONCHIP_FAST && !small_g)) refill();
         if (any || fold) {
@@ -658,7 +751,7 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                     if (key[i] >= 0) kc[i] = ktop_cur[key[i]];
             }
         }
-        since += TILE;
+        since += VTILE;
 
         // a3 + a4: digits under the group's current top, 32-bit shared atomics
         if (small_g) {

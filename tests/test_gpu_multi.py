@@ -1,0 +1,128 @@
+"""GPU parity of the multi-column GroupBy (repro_groupby_sum_multi): several
+SUMs + COUNT per key, fused into one on-chip pass for small group counts and
+run column by column otherwise, against the CPU oracle bit for bit."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle as O  # noqa: E402
+from paper_1802_09883_b200 import synth  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def R():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1802_09883_b200 as R
+    return R
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def check(R, keys, cols, G, K, proj, path=None):
+    outs, counts = R.groupby_sum_multi(dev(keys), [dev(c) for c in cols], G, K, proj=proj)
+    torch.cuda.synchronize()
+    if path is not None:
+        assert R.last_path() == path
+    rc, ref, ref_counts = O.groupby_sum_multi(keys, cols, G, K, proj=proj)
+    assert rc == O.OK
+    for o, r in zip(outs, ref):
+        assert o.cpu().numpy().tobytes() == r.tobytes()
+    assert np.array_equal(counts.cpu().numpy(), ref_counts)
+
+
+@pytest.mark.parametrize("n", [1, 1000, 3 * 512 * 7 + 13, 1 << 20])
+def test_config4_shape_fused(R, n):
+    keys, (qty, price, disc, tax) = synth.generate(4, n=n)
+    check(R, keys, [qty, price, disc, tax], 4, 3, 1, path=2)
+
+
+@pytest.mark.parametrize("K", [1, 2, 4])
+def test_config4_shape_other_folds(R, K):
+    keys, cols = synth.generate(4, n=200003)
+    check(R, keys, list(cols), 4, K, 1, path=2)
+
+
+@pytest.mark.parametrize("dtype,ncols,G", [(np.float64, 1, 7), (np.float64, 2, 100), (np.float64, 4, 200),
+                                           (np.float32, 1, 33), (np.float32, 2, 5), (np.float32, 4, 50)])
+def test_independent_columns_fused(R, dtype, ncols, G):
+    rng = np.random.default_rng(ncols * 1000 + G)
+    n = 300001
+    keys = rng.integers(0, G, n).astype(np.int32)
+    cols = [(rng.standard_normal(n) * 2.0 ** rng.integers(-20, 20, n)).astype(dtype) for _ in range(ncols)]
+    check(R, keys, cols, G, 3 if dtype == np.float64 else 2, 0, path=2)
+
+
+@pytest.mark.parametrize("proj,ncols,G", [(1, 4, 300), (0, 3, 10), (0, 2, 5000)])
+def test_column_by_column_fallback(R, proj, ncols, G):
+    rng = np.random.default_rng(G)
+    n = 250000
+    if proj == 1:
+        keys, cols = synth.generate(4, n=n, n_groups=G)
+        cols = list(cols)
+    else:
+        keys = rng.integers(0, G, n).astype(np.int32)
+        cols = [rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-40, 40, n) for _ in range(ncols)]
+    check(R, keys, cols, G, 3, proj, path=3)
+
+
+def test_unaligned_columns_take_register_loads(R):
+    keys, cols = synth.generate(4, n=100001)
+    # offset views: the columns are no longer 16-byte aligned (no TMA ring)
+    kd = dev(np.concatenate([np.zeros(1, np.int32), keys]))[1:]
+    cd = [dev(np.concatenate([[0.0], c]))[1:] for c in cols]
+    outs, counts = R.groupby_sum_multi(kd, cd, 4, 3, proj=1)
+    rc, ref, rc_counts = O.groupby_sum_multi(keys, list(cols), 4, 3, proj=1)
+    for o, r in zip(outs, ref):
+        assert o.cpu().numpy().tobytes() == r.tobytes()
+    assert np.array_equal(counts.cpu().numpy(), rc_counts)
+
+
+def test_multi_level_shifts_and_order_invariance(R):
+    rng = np.random.default_rng(3)
+    n = 400000
+    keys = rng.integers(0, 6, n).astype(np.int32)
+    cols = [rng.uniform(-1, 1, n) * 2.0 ** rng.integers(-200, 200, n) for _ in range(2)]
+    check(R, keys, cols, 6, 3, 0, path=2)
+    perm = rng.permutation(n)
+    a, _ = R.groupby_sum_multi(dev(keys), [dev(c) for c in cols], 6, 3)
+    b, _ = R.groupby_sum_multi(dev(keys[perm]), [dev(c[perm]) for c in cols], 6, 3)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+
+
+def test_multi_errors(R):
+    keys = np.zeros(5000, np.int32)
+    good = np.ones(5000)
+    bad = good.copy()
+    bad[1234] = np.nan
+    with pytest.raises(R.ReproError) as e:
+        R.groupby_sum_multi(dev(keys), [dev(good), dev(bad)], 2, 3)
+    assert e.value.status == R.EDOM
+    keys[77] = 9
+    with pytest.raises(R.ReproError) as e:
+        R.groupby_sum_multi(dev(keys), [dev(good), dev(bad)], 2, 3)
+    assert e.value.status == R.EKEY
+    with pytest.raises(R.ReproError) as e:  # projection needs 4 binary64 columns
+        R.groupby_sum_multi(dev(keys), [dev(good)] * 3, 2, 3, proj=1)
+    assert e.value.status == R.EINVAL
+
+
+def test_multi_async_matches_blocking(R):
+    keys, cols = synth.generate(4, n=123457)
+    kd, cd = dev(keys), [dev(c) for c in cols]
+    ws = R.make_multi_workspace(keys.size, 4, 4, 1, 3, R.F64)
+    st = torch.full((1,), 99, dtype=torch.int32, device="cuda")
+    outs = [torch.empty(4, dtype=torch.float64, device="cuda") for _ in range(4)]
+    counts = torch.empty(4, dtype=torch.int64, device="cuda")
+    R.groupby_sum_multi_async(kd, cd, 4, 3, 1, outs, counts, ws, st)
+    torch.cuda.synchronize()
+    assert st.item() == 0
+    ref, rc = R.groupby_sum_multi(kd, cd, 4, 3, proj=1)
+    for x, y in zip(outs, ref):
+        assert torch.equal(x, y)
+    assert torch.equal(counts, rc)
