@@ -99,6 +99,16 @@ int repro_groupby_sum_host(const int32_t *keys_host, const void *vals_host,
 /* Free the internal workspace cache of the blocking entry points. */
 void repro_release_cache(void);
 
+/* Bench / test support, not part of the method: the seeded synthetic input
+ * generator of paper_1802_09883_b200/synth.py run on the device (rows r0 ..
+ * r0+n of BASELINE config 0/1/2 -- one binary64 column -- or 4 -- columns
+ * qty, price, disc, tax), bit-identical to the numpy generator.  keys int32[n],
+ * cols: HOST array of DEVICE pointers.  Stream-ordered; EINVAL for other
+ * configs. */
+int repro_synth_generate(int32_t config, uint64_t seed, int64_t r0, int64_t n,
+                         int32_t n_groups, int32_t *keys, void *const *cols,
+                         void *stream);
+
 /* ------------------------------------------------------------------------
  * Several aggregates of one key column in one pass
  * ---------------------------------------------------------------------- */

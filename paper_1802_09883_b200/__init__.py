@@ -47,6 +47,7 @@ _sig("repro_groupby_workspace_bytes", _sz, _i64, _i32, _i32, _i32)
 _sig("repro_groupby_sum_async", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp)
 _sig("repro_groupby_sum_host", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp)
 _sig("repro_release_cache", None)
+_sig("repro_synth_generate", ctypes.c_int, _i32, ctypes.c_uint64, _i64, _i64, _i32, _vp, ctypes.POINTER(_vp), _vp)
 _sig("repro_groupby_sum_multi", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
      ctypes.POINTER(_vp), _vp)
 _sig("repro_groupby_multi_workspace_bytes", _sz, _i64, _i32, _i32, _i32, _i32, _i32)
@@ -243,6 +244,20 @@ def groupby_sum_multi_async(keys, cols, n_groups: int, fold: int, proj: int, out
                                             _dev(status, "status", torch.int32))
     _check(st, "repro_groupby_sum_multi_async")
     return outs
+
+
+def synth_generate(config: int, n: int, n_groups: int, r0: int = 0, seed: int | None = None, stream=None):
+    """Seeded synthetic inputs of BASELINE config 0/1/2/4 generated on the
+    device (same bits as synth.generate); returns (keys, [value columns])."""
+    torch = _torch()
+    from .synth import SEED_BASE
+    seed = SEED_BASE + config if seed is None else seed
+    keys = torch.empty(n, dtype=torch.int32, device="cuda")
+    cols = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(4 if config == 4 else 1)]
+    cptr = (_vp * len(cols))(*[_dev(c, "cols") for c in cols])
+    _check(_lib.repro_synth_generate(config, seed, r0, n, n_groups, _dev(keys, "keys", torch.int32), cptr,
+                                     _stream_ptr(stream)), "repro_synth_generate")
+    return keys, cols
 
 
 def baseline_atomic_sum(keys, vals, n_groups: int, variant: int = 0, accumulate_f64: bool = False, out=None,

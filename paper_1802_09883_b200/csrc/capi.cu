@@ -494,6 +494,16 @@ int repro_groupby_sum_multi(const int32_t *keys, const void *const *cols, int32_
     return finish_blocking(flags, 0);
 }
 
+int repro_synth_generate(int32_t config, uint64_t seed, int64_t r0, int64_t n, int32_t n_groups, int32_t *keys,
+                         void *const *cols, void *stream) {
+    if (n < 0 || n_groups < 1 || (n > 0 && (!keys || !cols))) return REPRO_EINVAL;
+    const int ncol = config == 4 ? 4 : 1;
+    for (int c = 0; c < ncol && n > 0; ++c)
+        if (!cols[c]) return REPRO_EINVAL;
+    const int rc = launch_synth(config, seed, r0, n, n_groups, keys, cols, (cudaStream_t)stream);
+    return rc == -1 ? REPRO_EINVAL : map_launch(rc);
+}
+
 void repro_release_cache(void) {
     std::lock_guard<std::mutex> lock(g_cache.mu);
     if (g_cache.ptr) cudaFree(g_cache.ptr);

@@ -49,6 +49,10 @@ int launch_q1_project(const double *price, const double *disc, const double *tax
 int launch_count_rows(const int32_t *keys, int64_t n, int32_t G, int64_t *counts, cudaStream_t st, int *launches);
 int launch_flags_or(uint32_t *acc, const uint32_t *f, cudaStream_t st, int *launches);
 
+// device copy of synth.py's seeded generator (bench/test support, k_synth.cu)
+int launch_synth(int config, uint64_t seed, int64_t r0, int64_t n, int32_t G, int32_t *keys, void *const *cols,
+                 cudaStream_t st);
+
 // slots (+ global tops) -> canonical state; optionally merged with the
 // existing state (acc_*), optionally finalised into out.  `merge` != 0 reads
 // acc_k/acc_C/acc_D as the previous state.

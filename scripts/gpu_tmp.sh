@@ -1,4 +1,6 @@
 cd $GRAFT_REPO_ROOT
-python scripts/check_variants.py 2>&1 | cut -c1-220
-for v in lane32; do echo $v; for g in 1 4 16 32; do REPRO_B200_LIB=$PWD/scripts/variants/lib_$v.so python scripts/stress_variant.py 4194304 $g; done; done
-NOCHECK=1 GROUPS_LIST=1,4,16,32,64 bash scripts/gpu_variants.sh; cat gpurun_out/variants.log | cut -c1-250
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_synth.py -q 2>&1 | tail -2
+timeout 900 python bench.py --config 4 --steps 10 --warmup 3 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo "rc=$?"; tail -3 gpurun_out/bench_c4.err
+timeout 900 python bench.py --steps 100 --warmup 5 > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err; echo "rc=$?"; tail -3 gpurun_out/bench_c1.err
+cat gpurun_out/bench_c4.json gpurun_out/bench_c1.json
