@@ -49,7 +49,7 @@ WORKLOADS = {
     4: "config4: 2^30 rows, keys U[0,4), fp64 qty/price/disc/tax, 4 repro SUMs (qty, price, price*(1-disc), "
        "price*(1-disc)*(1+tax)) + COUNT, K=3 (fused multi-column pass)",
 }
-ORACLE_SAMPLE_ROWS = 1 << 26  # bounded oracle sample (cpu_baseline / reference arm), ~10-30 s of host work
+ORACLE_SAMPLE_ROWS = 1 << 27  # bounded oracle sample (cpu_baseline): <= 2^27 rows, well under 30 s of host work
 PARITY_ROWS_MULTI = 1 << 24   # config 4: rows of the full input re-run on both sides for the parity check
 
 
