@@ -1,22 +1,29 @@
 // k_partition.cu -- high-cardinality path:
 // PartitionAndAggregate (Alg. 4) on the GPU.
 //
-//   1. k_part_hist     per-block histogram of partition ids p = key >> s
-//                      (contiguous key ranges of Gp = 2^s groups), EKEY check
-//   2. k_part_colscan  per partition: offsets of every block inside it
-//   3. k_part_plan     exclusive scan of partition sizes; split every
-//                      partition into work items of <= CH rows (so skewed
-//                      partitions are shared by many blocks)
-//   4. k_part_scatter  rows -> partition order (ParallelPartition, PAPER.md:
-//                      1054-1065; the order inside a partition is irrelevant
-//                      because the accumulator is associative)
-//   5. k_part_accumulate persistent blocks pull work items and run the
-//                      on-chip table code (onchip_core.cuh) on Gp local groups,
-//                      writing one partial state per (item, group)
-//   6. k_part_merge    per group: max of the items' window tops, realign, add
-//                      (the shared-table merge of Alg. 4 lines 6-9 via
-//                      operator+=(repro)), canonicalise,
-//                      Eq. 1 read-out / merge into an accumulator.
+// Rows are radix-partitioned by partition id p = key >> 10 (contiguous key
+// ranges of 1024 groups, one on-chip table each), most significant digit
+// first, with at most 2^7 digits per pass (ParallelPartition with F = f^d,
+// one pass for <= 128 partitions, two otherwise), each
+// pass over SEGMENTS (the previous pass's partitions; the first pass has one):
+//   1. k_seg_units    split every segment into units of <= CU rows
+//   2. k_seg_hist     per unit: digit histogram (warp multisplit by ballots,
+//                     per-warp counts, no shared atomics); EKEY check
+//   3. k_seg_scan     per (segment, digit): unit offsets and totals
+//   4. k_part_plan    exclusive scan of the totals = output bases; after the
+//                     last pass also the work items of step 5 (<= CH rows,
+//                     so skewed partitions are shared by many blocks)
+//   5. k_seg_scatter  per unit, per 4096-row tile: warp multisplit ranks,
+//                     block scan, shared staging in digit order, coalesced
+//                     runs to the output (the order inside a partition is
+//                     irrelevant: the accumulator is associative)
+//   6. k_part_accumulate  persistent blocks pull work items and run the
+//                     on-chip table code (onchip_core.cuh) on 1024 local
+//                     groups, writing one partial state per (item, group)
+//   7. k_part_merge   per group: max of the items' window tops, realign, add
+//                     (the shared-table merge of Alg. 4 lines 6-9 via
+//                     operator+=(repro)), canonicalise,
+//                     Eq. 1 read-out / merge into an accumulator.
 // Each group lives in exactly one partition, so no group is merged across
 // partitions.
 #include "common.cuh"
@@ -32,40 +39,81 @@ namespace {
 constexpr int PART_LOG_GP = 10;               // Gp = 1024 groups per partition
 constexpr int PART_GP = 1 << PART_LOG_GP;
 constexpr int64_t PART_CH = 1 << 14;          // minimum rows per work item
-constexpr int HIST_TPB = 512;
+constexpr int SEG_TPB = 256;                 // hist / scatter blocks
+constexpr int SEG_NW = SEG_TPB / 32;
+constexpr int SEG_RT = 8;                    // rows per thread per scatter tile
+#ifndef SEG_RTH
+#define SEG_RTH 32                           // keys per thread in flight in the histogram
+#endif
+#ifndef SEG_ONEPASS_BITS64
+#define SEG_ONEPASS_BITS64 8                 // binary64 rows: one pass up to 2^this partitions
+#endif
+#ifndef SEG_ONEPASS_BITS32
+#define SEG_ONEPASS_BITS32 10                // binary32 rows (wide scatter above 2^8)
+#endif
+constexpr int SEG_TILE = SEG_TPB * SEG_RT;   // 2048
+constexpr int SEG_MAX_BITS = 8;             // multisplit scatter / lane histograms: digits per pass <= 2^this
+constexpr int SEG_FMAX = 1 << SEG_MAX_BITS;
+static_assert(SEG_MAX_BITS <= 8, "scatter stages digits as bytes");
 constexpr size_t PALIGN = 256;
 
 inline size_t al(size_t x) { return (x + PALIGN - 1) / PALIGN * PALIGN; }
 
 struct Plan {
-    int64_t ch;     // rows per work item
-    int P;          // partitions
-    int B;          // histogram / scatter blocks
-    int64_t chunk;  // rows per histogram block
+    int64_t ch;      // rows per work item (accumulate)
+    int P;           // partitions holding groups: ceil(G / 1024)
+    int pbits;       // log2 of the padded partition count Pf
+    int Pf;          // 1 << pbits
+    int passes;      // 1 or 2
+    int bits[2];     // digit bits per pass
+    int shift[2];    // digit = (key >> shift) & ((1 << bits) - 1)
+    int64_t cu;      // rows per unit
+    int64_t max_units;
     int64_t max_items;
+    int grid;        // persistent blocks of the hist / scatter kernels
 };
 
-Plan make_plan(int64_t n, int32_t G) {
+Plan make_plan(int64_t n, int32_t G, int DT) {
     Plan pl;
     pl.P = (int)(((int64_t)G + PART_GP - 1) >> PART_LOG_GP);
-    pl.B = std::max(1, std::min<int>(2 * device_props().sms, (int)((n + 65535) / 65536)));
-    pl.chunk = (n + pl.B - 1) / pl.B;
-    pl.chunk = (pl.chunk + 3) / 4 * 4;
-    if (pl.chunk == 0) pl.chunk = 4;
-    pl.B = (int)std::max<int64_t>(1, (n + pl.chunk - 1) / pl.chunk);
+    pl.pbits = 0;
+    while ((1 << pl.pbits) < pl.P) ++pl.pbits;
+    pl.Pf = 1 << pl.pbits;
+    if (pl.pbits <= (DT == 1 ? SEG_ONEPASS_BITS64 : SEG_ONEPASS_BITS32)) {
+        pl.passes = 1;
+        pl.bits[0] = pl.pbits;
+        pl.shift[0] = PART_LOG_GP;
+        pl.bits[1] = 0;
+        pl.shift[1] = 0;
+    } else {
+        pl.passes = 2;
+        pl.bits[1] = (pl.pbits + 1) / 2;
+        pl.bits[0] = pl.pbits - pl.bits[1];
+        pl.shift[0] = PART_LOG_GP + pl.bits[1];
+        pl.shift[1] = PART_LOG_GP;
+    }
+    const int sms = device_props().sms;
+    pl.cu = std::max<int64_t>(1 << 14, (n + 8 * sms - 1) / (8 * sms));
+    pl.max_units = (n + pl.cu - 1) / pl.cu + (1 << pl.bits[0]) + 1;
+    pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * sms, pl.max_units));
     // work items: ~8 per SM over the whole input, at least PART_CH rows
-    pl.ch = std::max<int64_t>(PART_CH, (n + 8 * device_props().sms - 1) / (8 * device_props().sms));
-    pl.max_items = (n + pl.ch - 1) / pl.ch + pl.P;
+    pl.ch = std::max<int64_t>(PART_CH, (n + 8 * sms - 1) / (8 * sms));
+    pl.max_items = (n + pl.ch - 1) / pl.ch + pl.Pf;
     return pl;
 }
 
 struct PartWs {
-    int32_t *pkeys;
+    int32_t *pkeys;   // final partitioned rows (local keys)
     void *pvals;
-    uint32_t *hist;   // [B][P]
-    int64_t *ptot;    // [P]    partition sizes
-    int64_t *base;    // [P+1]  first row of each partition
-    int64_t *pitem;   // [P+1]  first work item of each partition
+    int32_t *akeys;   // first-pass output of a two-pass plan (full keys)
+    void *avals;
+    uint32_t *hist;   // [max_units][2^bits] unit offsets per digit
+    int64_t *units;   // [max_units][2] row range
+    int32_t *useg;    // [max_units] segment of each unit
+    int32_t *ufirst;  // [2^bits0 + 2] first unit of each segment (+ count)
+    int64_t *ptot;    // [Pf]    partition sizes
+    int64_t *base;    // [Pf+1]  first row of each partition
+    int64_t *pitem;   // [Pf+1]  first work item of each partition
     int64_t *items;   // [max_items][2] row range
     int32_t *iown;    // [max_items] partition of each item
     int32_t *ctrl;    // [0] number of items, [1] work-queue head
@@ -80,12 +128,20 @@ PartWs carve(void *ws, int64_t n, int32_t G, int K, int DT, const Plan &pl) {
     size_t o = 0;
     const size_t vsz = DT == 1 ? 8 : 4;
     auto take = [&](size_t bytes) { char *p = b + o; o += al(bytes); return p; };
+    const int fmax = 1 << std::max(pl.bits[0], pl.bits[1]);
     w.pkeys = (int32_t *)take(4 * (size_t)n + 16);
     w.pvals = take(vsz * (size_t)n + 16);
-    w.hist = (uint32_t *)take(4 * (size_t)pl.B * pl.P);
-    w.ptot = (int64_t *)take(8 * (size_t)pl.P);
-    w.base = (int64_t *)take(8 * ((size_t)pl.P + 1));
-    w.pitem = (int64_t *)take(8 * ((size_t)pl.P + 1));
+    if (pl.passes == 2) {
+        w.akeys = (int32_t *)take(4 * (size_t)n + 16);
+        w.avals = take(vsz * (size_t)n + 16);
+    }
+    w.hist = (uint32_t *)take(4 * (size_t)pl.max_units * fmax);  // fmax <= 2^SEG_ONEPASS_BITS
+    w.units = (int64_t *)take(16 * (size_t)pl.max_units);
+    w.useg = (int32_t *)take(4 * (size_t)pl.max_units);
+    w.ufirst = (int32_t *)take(4 * ((size_t)(1 << pl.bits[0]) + 2));
+    w.ptot = (int64_t *)take(8 * (size_t)pl.Pf);
+    w.base = (int64_t *)take(8 * ((size_t)pl.Pf + 1));
+    w.pitem = (int64_t *)take(8 * ((size_t)pl.Pf + 1));
     w.items = (int64_t *)take(16 * (size_t)pl.max_items);
     w.iown = (int32_t *)take(4 * (size_t)pl.max_items);
     w.ctrl = (int32_t *)take(16);
@@ -95,46 +151,150 @@ PartWs carve(void *ws, int64_t n, int32_t G, int K, int DT, const Plan &pl) {
     return w;
 }
 
-__global__ void __launch_bounds__(HIST_TPB)
-k_part_hist(const int32_t *__restrict__ keys, int64_t n, int32_t G, int P, int64_t chunk, uint32_t *hist,
-            uint32_t *status) {
-    extern __shared__ uint32_t bins[];
-    for (int p = threadIdx.x; p < P; p += HIST_TPB) bins[p] = 0;
-    __syncthreads();
-    const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);  // r0 % 4 == 0
-    uint32_t bad = 0;
-    const int64_t v1 = r0 + ((r1 - r0) & ~(int64_t)3);
-    for (int64_t r = r0 + 4 * (int64_t)threadIdx.x; r < v1; r += 4 * HIST_TPB) {
-        const int4 k4 = __ldg(reinterpret_cast<const int4 *>(keys + r));
-        const int kk[4] = {k4.x, k4.y, k4.z, k4.w};
+// ---- segmented radix passes ------------------------------------------------
+
+// Units: segment s = rows [base[s], base[s+1]) (base == nullptr: one segment
+// [0, n)) split into ceil(len / cu) units.  Single block.
+__global__ void __launch_bounds__(1024) k_seg_units(const int64_t *base, int S, int64_t n, int64_t cu, int64_t *units,
+                                                    int32_t *useg, int32_t *ufirst) {
+    __shared__ int32_t wsum[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int per = (S + 1023) / 1024;
+    const int s0 = min(tid * per, S), s1 = min(s0 + per, S);
+    auto seg = [&](int s, int64_t &a, int64_t &b) {
+        a = base ? base[s] : 0;
+        b = base ? base[s + 1] : n;
+    };
+    int cnt = 0;
+    for (int s = s0; s < s1; ++s) {
+        int64_t a, b;
+        seg(s, a, b);
+        cnt += (int)((b - a + cu - 1) / cu);
+    }
+    int incl = cnt;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if ((uint32_t)kk[j] < (uint32_t)G) atomicAdd(&bins[kk[j] >> PART_LOG_GP], 1u);
-            else bad = FLAG_EKEY;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) wsum[warp] = incl;
+    __syncthreads();
+    int u = incl - cnt;
+    for (int w = 0; w < warp; ++w) u += wsum[w];
+    for (int s = s0; s < s1; ++s) {
+        int64_t a, b;
+        seg(s, a, b);
+        ufirst[s] = u;
+        for (int64_t r = a; r < b; r += cu, ++u) {
+            units[2 * u] = r;
+            units[2 * u + 1] = min(b, r + cu);
+            useg[u] = s;
         }
     }
-    for (int64_t r = v1 + threadIdx.x; r < r1; r += HIST_TPB) {
-        const int k = __ldg(keys + r);
-        if ((uint32_t)k < (uint32_t)G) atomicAdd(&bins[k >> PART_LOG_GP], 1u);
-        else bad = FLAG_EKEY;
+    if (tid == 1023) {
+        ufirst[S] = u;      // total units
+        ufirst[S + 1] = u;
     }
-    __syncthreads();
-    for (int p = threadIdx.x; p < P; p += HIST_TPB) hist[(size_t)blockIdx.x * P + p] = bins[p];
-    bad = __reduce_or_sync(0xffffffffu, bad);
-    if ((threadIdx.x & 31) == 0 && bad) atomicOr(status, bad);
 }
 
-// per partition p: hist[b][p] <- rows of p in blocks < b; ptot[p] <- total
-__global__ void k_part_colscan(uint32_t *hist, int B, int P, int64_t *ptot) {
-    const int p = blockIdx.x * blockDim.x + threadIdx.x;
-    if (p >= P) return;
-    int64_t run = 0;
-    for (int b = 0; b < B; ++b) {
-        const uint32_t c = hist[(size_t)b * P + p];
-        hist[(size_t)b * P + p] = (uint32_t)run;
-        run += c;
+// Warp multisplit of one 32-row slot: lanes whose `ok` is set and whose digit
+// d (bits bits) is equal form one peer set (mask from one ballot per bit);
+// returns the peer mask.
+__device__ __forceinline__ uint32_t peers_of(int d, int bits, bool ok) {
+    uint32_t m = __ballot_sync(0xffffffffu, ok);
+    for (int b = 0; b < bits; ++b) {
+        const bool bit = (d >> b) & 1;
+        const uint32_t bb = __ballot_sync(0xffffffffu, bit);
+        m &= bit ? bb : ~bb;
     }
-    ptot[p] = run;
+    return ok ? m : 0u;
+}
+
+// Digit histogram per unit.  F <= 32: one private counter row per lane
+// (counter [warp][d][lane], always bank = lane: plain load-add-store, no
+// atomics, no conflicts); F > 32: per-warp histograms with shared atomics.
+// Both are summed over lanes / warps at the end of the unit.  The first pass
+// also checks the keys against [0, G).
+__global__ void __launch_bounds__(SEG_TPB)
+k_seg_hist(const int32_t *__restrict__ keys, const int64_t *__restrict__ units, const int32_t *__restrict__ ufirst,
+           int S, int shift, int bits, int32_t G, int check, uint32_t *hist, uint32_t *status) {
+    __shared__ uint32_t h[SEG_NW * 32 * 32];  // lane rows (F <= 32) or [NW][F] (F > 32): 32 KB
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int F = 1 << bits;
+    const bool lanes = F <= 32;
+    const int nunits = ufirst[S];
+    uint32_t *hw = lanes ? h + warp * 32 * 32 : h + warp * F;
+    uint32_t bad = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        for (int i = tid; i < SEG_NW * 32 * 32; i += SEG_TPB) h[i] = 0;
+        __syncthreads();
+        const int64_t a = units[2 * u], b = units[2 * u + 1];
+        for (int64_t r0 = a + warp * 32 * SEG_RTH; r0 < b; r0 += SEG_NW * 32 * SEG_RTH) {
+            int kk[SEG_RTH];  // SEG_RTH warp slots in flight per thread
+#pragma unroll
+            for (int j = 0; j < SEG_RTH; ++j) {
+                const int64_t r = r0 + j * 32 + lane;
+                kk[j] = r < b ? __ldg(keys + r) : -1;
+                if (check && r < b && (uint32_t)kk[j] >= (uint32_t)G) bad = FLAG_EKEY;
+            }
+#pragma unroll
+            for (int j = 0; j < SEG_RTH; ++j) {
+                if ((uint32_t)kk[j] < (uint32_t)G) {
+                    const int d = (kk[j] >> shift) & (F - 1);
+                    if (lanes) hw[d * 32 + lane] += 1u;
+                    else atomicAdd(&hw[d], 1u);
+                }
+            }
+        }
+        __syncthreads();
+        for (int d = tid; d < F; d += SEG_TPB) {
+            uint32_t t = 0;
+            if (lanes) {
+                for (int w = 0; w < SEG_NW; ++w)
+                    for (int l = 0; l < 32; ++l) t += h[w * 1024 + d * 32 + ((l + d) & 31)];
+            } else {
+                for (int w = 0; w < SEG_NW; ++w) t += h[w * F + d];
+            }
+            hist[(size_t)u * F + d] = t;
+        }
+        __syncthreads();
+    }
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if (lane == 0 && bad) atomicOr(status, bad);
+}
+
+// per (segment s, digit d), one block each: hist[u][d] <- rows of digit d in
+// the units of s before u (block-wide scan over the units, 256 at a time);
+// ptot[s * F + d] <- total
+__global__ void __launch_bounds__(256) k_seg_scan(uint32_t *hist, const int32_t *__restrict__ ufirst, int bits,
+                                                  int64_t *ptot) {
+    __shared__ int64_t wsum[8];
+    const int F = 1 << bits;
+    const int s = blockIdx.x / F, d = blockIdx.x - s * F;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int u0 = ufirst[s], u1 = ufirst[s + 1];
+    int64_t run = 0;
+    for (int c = u0; c < u1; c += 256) {
+        const int u = c + tid;
+        const int64_t v = u < u1 ? hist[(size_t)u * F + d] : 0;
+        int64_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        int64_t pre = run + incl - v, tot = 0;
+        for (int w = 0; w < 8; ++w) {
+            if (w < warp) pre += wsum[w];
+            tot += wsum[w];
+        }
+        if (u < u1) hist[(size_t)u * F + d] = (uint32_t)pre;
+        run += tot;
+        __syncthreads();
+    }
+    if (tid == 0) ptot[blockIdx.x] = run;
 }
 
 // single block: base[] = exclusive scan of ptot, pitem[] = exclusive scan of
@@ -180,133 +340,217 @@ __global__ void __launch_bounds__(1024) k_part_plan(const int64_t *ptot, int P, 
     }
 }
 
-// Direct scatter (one 32-bit shared cursor per partition): best when there
-// are very few partitions (runs are long anyway) or too many to stage.
+// Scatter one pass: per unit (persistent blocks), per tile of SEG_TILE rows:
+// every row's rank among the tile's rows of its digit from the warp
+// multisplit (per-warp running counts, no shared atomics), a block scan over
+// (digit, warp), staging in digit order in shared memory, then coalesced runs
+// to cursor[d] (output base of (segment, digit) + the unit's offset).  LOCAL:
+// write the key within its 1024-group partition (last pass).
 template <typename V>
-__global__ void __launch_bounds__(HIST_TPB)
-k_part_scatter_direct(const int32_t *__restrict__ keys, const V *__restrict__ vals, int64_t n, int32_t G, int P,
-                      int64_t chunk, const uint32_t *hist, const int64_t *base, int32_t *pkeys, V *pvals) {
-    extern __shared__ uint32_t cursor_d[];
-    for (int p = threadIdx.x; p < P; p += HIST_TPB)
-        cursor_d[p] = (uint32_t)(base[p] + hist[(size_t)blockIdx.x * P + p]);
-    __syncthreads();
-    const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);  // r0 % 4 == 0
-    const int64_t v1 = r0 + ((r1 - r0) & ~(int64_t)3);
-    for (int64_t r = r0 + 4 * (int64_t)threadIdx.x; r < v1; r += 4 * HIST_TPB) {
-        const int4 k4 = __ldg(reinterpret_cast<const int4 *>(keys + r));
-        const int kk[4] = {k4.x, k4.y, k4.z, k4.w};
-        V vv[4];
+__global__ void __launch_bounds__(SEG_TPB)
+k_seg_scatter(const int32_t *__restrict__ ikeys, const V *__restrict__ ivals, const int64_t *__restrict__ units,
+              const int32_t *__restrict__ useg, const int32_t *__restrict__ ufirst, int S, int shift, int bits,
+              int32_t G, int local, const uint32_t *__restrict__ hist, const int64_t *__restrict__ obase,
+              int32_t *__restrict__ okeys, V *__restrict__ ovals) {
+    constexpr int TPB = SEG_TPB, NW = SEG_NW, RT = SEG_RT, TILE = SEG_TILE;
+    extern __shared__ __align__(16) unsigned char sm[];
+    V *sval = reinterpret_cast<V *>(sm);                          // [TILE]
+    int32_t *skey = reinterpret_cast<int32_t *>(sval + TILE);     // [TILE]
+    uint8_t *sdig = reinterpret_cast<uint8_t *>(skey + TILE);     // [TILE]
+    uint32_t *wh = reinterpret_cast<uint32_t *>(sdig + TILE);     // [NW][FMAX] running counts, then offsets
+    uint32_t *tot = wh + NW * SEG_FMAX;                           // [FMAX] tile totals
+    uint32_t *tstart = tot + SEG_FMAX;                            // [FMAX] tile start of each digit
+    int64_t *cursor = reinterpret_cast<int64_t *>(tstart + SEG_FMAX);  // [FMAX]
+    uint32_t *wsc = reinterpret_cast<uint32_t *>(cursor + SEG_FMAX);   // [32] scan scratch
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int F = 1 << bits;
+    const int nunits = ufirst[S];
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int s = useg[u];
+        for (int d = tid; d < F; d += TPB) cursor[d] = obase[(size_t)s * F + d] + hist[(size_t)u * F + d];
+        const int64_t a = units[2 * u], b = units[2 * u + 1];
+        for (int64_t t0 = a; t0 < b; t0 += TILE) {
+            for (int d = lane; d < F; d += 32) wh[warp * SEG_FMAX + d] = 0;
+            __syncwarp();
+            int kk[RT], dd[RT];
+            uint32_t rk[RT];
+            V vv[RT];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) vv[j] = __ldg(vals + r + j);
+            for (int j = 0; j < RT; ++j) {
+                const int64_t r = t0 + (int64_t)(j * NW + warp) * 32 + lane;  // warp-contiguous 32-row slots
+                kk[j] = -1;
+                vv[j] = V(0);
+                if (r < b) {
+                    kk[j] = __ldg(ikeys + r);
+                    vv[j] = __ldg(ivals + r);
+                }
+            }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            if ((uint32_t)kk[j] >= (uint32_t)G) continue;
-            const uint32_t pos = atomicAdd(&cursor_d[kk[j] >> PART_LOG_GP], 1u);
-            pkeys[pos] = kk[j] & (PART_GP - 1);
-            pvals[pos] = vv[j];
+            for (int j = 0; j < RT; ++j) {
+                const bool valid = (uint32_t)kk[j] < (uint32_t)G;
+                dd[j] = valid ? (kk[j] >> shift) & (F - 1) : 0;
+                const uint32_t m = peers_of(dd[j], bits, valid);
+                const uint32_t before = valid ? wh[warp * SEG_FMAX + dd[j]] : 0u;
+                rk[j] = valid ? before + __popc(m & ((1u << lane) - 1u)) : 0xFFFFFFFFu;
+                __syncwarp();
+                if (valid && (m & ((1u << lane) - 1u)) == 0u) wh[warp * SEG_FMAX + dd[j]] = before + __popc(m);
+                __syncwarp();
+            }
+            __syncthreads();
+            // exclusive scan over (digit, warp): wh[w][d] <- tile offset of
+            // warp w's rows of digit d; tstart[d], tot[d]
+            const int per = (F * NW + TPB - 1) / TPB;  // entries per thread, digit-major order
+            const int e0 = min(tid * per, F * NW), e1 = min(e0 + per, F * NW);
+            uint32_t loc = 0;
+            for (int e = e0; e < e1; ++e) loc += wh[(e % NW) * SEG_FMAX + e / NW];
+            uint32_t incl = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) wsc[warp] = incl;
+            __syncthreads();
+            uint32_t run = incl - loc;
+            for (int w = 0; w < warp; ++w) run += wsc[w];
+            for (int e = e0; e < e1; ++e) {
+                const int d = e / NW, w = e % NW;
+                const uint32_t c = wh[w * SEG_FMAX + d];
+                if (w == 0) tstart[d] = run;
+                wh[w * SEG_FMAX + d] = run;
+                run += c;
+            }
+            __syncthreads();
+            uint32_t ntile = 0;
+            for (int w = 0; w < NW; ++w) ntile += wsc[w];
+            for (int d = tid; d < F; d += TPB) tot[d] = (d + 1 < F ? tstart[d + 1] : ntile) - tstart[d];
+#pragma unroll
+            for (int j = 0; j < RT; ++j) {
+                if (rk[j] == 0xFFFFFFFFu) continue;
+                const uint32_t q = wh[warp * SEG_FMAX + dd[j]] + rk[j];
+                sval[q] = vv[j];
+                skey[q] = local ? (kk[j] & (PART_GP - 1)) : kk[j];
+                sdig[q] = (uint8_t)dd[j];
+            }
+            __syncthreads();
+            for (uint32_t q = tid; q < ntile; q += TPB) {
+                const int d = sdig[q];
+                const int64_t pos = cursor[d] + (q - tstart[d]);
+                okeys[pos] = skey[q];
+                ovals[pos] = sval[q];
+            }
+            __syncthreads();
+            for (int d = tid; d < F; d += TPB) cursor[d] += tot[d];
+            __syncthreads();
         }
-    }
-    for (int64_t r = v1 + threadIdx.x; r < r1; r += HIST_TPB) {
-        const int k = __ldg(keys + r);
-        if ((uint32_t)k >= (uint32_t)G) continue;
-        const uint32_t pos = atomicAdd(&cursor_d[k >> PART_LOG_GP], 1u);
-        pkeys[pos] = k & (PART_GP - 1);
-        pvals[pos] = __ldg(vals + r);
     }
 }
 
-// Scatter with tile-local sorting: each tile of SC_TILE rows is first grouped
-// by partition in shared memory (rank from a shared histogram, offsets from a
-// block scan), then written out so that consecutive threads store consecutive
-// rows of the same partition (coalesced runs instead of one line per lane).
-constexpr int SC_TPB = 512;
-constexpr int SC_R = 8;
-constexpr int SC_TILE = SC_TPB * SC_R;
+// Wide-fan-out scatter (F > 2^SEG_MAX_BITS, single pass): ranks inside the
+// tile from shared-memory atomics on per-digit counters (fine when F is large:
+// few lanes share a counter), block scan over the digits, staging in digit
+// order, coalesced runs to the output.
+constexpr int WS_TPB = 512;
+constexpr int WS_R = 8;
+constexpr int WS_TILE = WS_TPB * WS_R;
 
 template <typename V>
-struct ScatterSmem {
-    // [P] per-partition: next global row of this block, tile count, tile start
-    static size_t bytes(int P) { return (size_t)12 * P + 64 * 4 + (size_t)SC_TILE * (sizeof(V) + 4 + 2) + 64; }
-};
+constexpr size_t seg_scatter_wide_smem(int F) {
+    return (size_t)12 * F + 64 * 4 + (size_t)WS_TILE * (sizeof(V) + 4 + 2) + 64;
+}
 
 template <typename V>
-__global__ void __launch_bounds__(SC_TPB)
-k_part_scatter(const int32_t *__restrict__ keys, const V *__restrict__ vals, int64_t n, int32_t G, int P,
-               int64_t chunk, const uint32_t *hist, const int64_t *base, int32_t *pkeys, V *pvals) {
+__global__ void __launch_bounds__(WS_TPB)
+k_seg_scatter_wide(const int32_t *__restrict__ ikeys, const V *__restrict__ ivals, const int64_t *__restrict__ units,
+                   const int32_t *__restrict__ useg, const int32_t *__restrict__ ufirst, int S, int shift, int bits,
+                   int32_t G, int local, const uint32_t *__restrict__ hist, const int64_t *__restrict__ obase,
+                   int32_t *__restrict__ okeys, V *__restrict__ ovals) {
     extern __shared__ __align__(16) unsigned char sm[];
-    uint32_t *cursor = reinterpret_cast<uint32_t *>(sm);  // [P] global row (n < 2^32)
-    uint32_t *tcnt = cursor + P;                           // [P] rows of the tile per partition
-    uint32_t *tstart = tcnt + P;                           // [P] tile-local start
-    uint32_t *wsum = tstart + P;                           // [32] scan scratch
-    V *sval = reinterpret_cast<V *>(sm + (((size_t)12 * P + 64 * 4 + 15) & ~(size_t)15));
-    int32_t *skey = reinterpret_cast<int32_t *>(sval + SC_TILE);
-    uint16_t *spart = reinterpret_cast<uint16_t *>(skey + SC_TILE);
+    const int F = 1 << bits;
+    uint32_t *cursor = reinterpret_cast<uint32_t *>(sm);  // [F] next output row (n < 2^32)
+    uint32_t *tcnt = cursor + F;                           // [F] rows of the tile per digit
+    uint32_t *tstart = tcnt + F;                           // [F] tile-local start
+    uint32_t *wsum = tstart + F;                           // [32] scan scratch
+    V *sval = reinterpret_cast<V *>(sm + (((size_t)12 * F + 64 * 4 + 15) & ~(size_t)15));
+    int32_t *skey = reinterpret_cast<int32_t *>(sval + WS_TILE);
+    uint16_t *sdig = reinterpret_cast<uint16_t *>(skey + WS_TILE);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    for (int p = tid; p < P; p += SC_TPB) {
-        cursor[p] = (uint32_t)(base[p] + hist[(size_t)blockIdx.x * P + p]);
-        tcnt[p] = 0;
-    }
-    __syncthreads();
-    const int cper = (P + SC_TPB - 1) / SC_TPB;
-    const int s0 = min(tid * cper, P), s1 = min(s0 + cper, P);
-    const int64_t r0 = (int64_t)blockIdx.x * chunk, r1 = min(n, r0 + chunk);
-    for (int64_t tb = r0; tb < r1; tb += SC_TILE) {
-        int kk[SC_R], pp[SC_R];
-        uint32_t rk[SC_R];
-        V vv[SC_R];
+    const int cper = (F + WS_TPB - 1) / WS_TPB;
+    const int s0 = min(tid * cper, F), s1 = min(s0 + cper, F);
+    const int nunits = ufirst[S];
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int sg = useg[u];
+        for (int d = tid; d < F; d += WS_TPB) {
+            cursor[d] = (uint32_t)(obase[(size_t)sg * F + d] + hist[(size_t)u * F + d]);
+            tcnt[d] = 0;
+        }
+        __syncthreads();
+        const int64_t a = units[2 * u], b = units[2 * u + 1];
+        for (int64_t tb = a; tb < b; tb += WS_TILE) {
+            int kk[WS_R], dd[WS_R];
+            uint32_t rk[WS_R];
+            V vv[WS_R];
 #pragma unroll
-        for (int i = 0; i < SC_R; ++i) {
-            const int64_t r = tb + (int64_t)i * SC_TPB + tid;
-            kk[i] = -1;
-            if (r < r1) {
-                kk[i] = __ldg(keys + r);
-                vv[i] = __ldg(vals + r);
+            for (int i = 0; i < WS_R; ++i) {
+                const int64_t r = tb + (int64_t)i * WS_TPB + tid;
+                kk[i] = -1;
+                vv[i] = V(0);
+                if (r < b) {
+                    kk[i] = __ldg(ikeys + r);
+                    vv[i] = __ldg(ivals + r);
+                }
             }
-            pp[i] = (uint32_t)kk[i] < (uint32_t)G ? (kk[i] >> PART_LOG_GP) : -1;
-            rk[i] = pp[i] >= 0 ? atomicAdd(&tcnt[pp[i]], 1u) : 0u;
-        }
-        __syncthreads();
-        // exclusive scan of the tile counts over the partitions
-        uint32_t local = 0;
-        for (int p = s0; p < s1; ++p) { tstart[p] = local; local += tcnt[p]; }
-        uint32_t incl = local;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) wsum[warp] = incl;
-        __syncthreads();
-        uint32_t pre = incl - local;
-        for (int w = 0; w < warp; ++w) pre += wsum[w];
-        for (int p = s0; p < s1; ++p) tstart[p] += pre;
-        __syncthreads();
-        const uint32_t nvalid = wsum[SC_TPB / 32 - 1] + 0;  // total rows of the tile with a valid key
-        uint32_t total = 0;
-        for (int w = 0; w < SC_TPB / 32; ++w) total += wsum[w];
-        (void)nvalid;
+            for (int i = 0; i < WS_R; ++i) {
+                dd[i] = (uint32_t)kk[i] < (uint32_t)G ? (kk[i] >> shift) & (F - 1) : -1;
+                rk[i] = dd[i] >= 0 ? atomicAdd(&tcnt[dd[i]], 1u) : 0u;
+            }
+            __syncthreads();
+            uint32_t loc = 0;
+            for (int d = s0; d < s1; ++d) { tstart[d] = loc; loc += tcnt[d]; }
+            uint32_t incl = loc;
 #pragma unroll
-        for (int i = 0; i < SC_R; ++i) {
-            if (pp[i] < 0) continue;
-            const uint32_t q = tstart[pp[i]] + rk[i];
-            sval[q] = vv[i];
-            skey[q] = kk[i] & (PART_GP - 1);
-            spart[q] = (uint16_t)pp[i];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) wsum[warp] = incl;
+            __syncthreads();
+            uint32_t pre = incl - loc;
+            for (int w = 0; w < warp; ++w) pre += wsum[w];
+            for (int d = s0; d < s1; ++d) tstart[d] += pre;
+            __syncthreads();
+            uint32_t total = 0;
+            for (int w = 0; w < WS_TPB / 32; ++w) total += wsum[w];
+#pragma unroll
+            for (int i = 0; i < WS_R; ++i) {
+                if (dd[i] < 0) continue;
+                const uint32_t q = tstart[dd[i]] + rk[i];
+                sval[q] = vv[i];
+                skey[q] = local ? (kk[i] & (PART_GP - 1)) : kk[i];
+                sdig[q] = (uint16_t)dd[i];
+            }
+            __syncthreads();
+            for (uint32_t q = tid; q < total; q += WS_TPB) {
+                const int d = sdig[q];
+                const uint32_t pos = cursor[d] + (q - tstart[d]);
+                okeys[pos] = skey[q];
+                ovals[pos] = sval[q];
+            }
+            __syncthreads();
+            for (int d = s0; d < s1; ++d) {
+                cursor[d] += tcnt[d];
+                tcnt[d] = 0;
+            }
+            __syncthreads();
         }
-        __syncthreads();
-        for (uint32_t q = tid; q < total; q += SC_TPB) {
-            const int p = spart[q];
-            const uint32_t pos = cursor[p] + (q - tstart[p]);
-            pkeys[pos] = skey[q];
-            pvals[pos] = sval[q];
-        }
-        __syncthreads();
-        for (int p = s0; p < s1; ++p) {
-            cursor[p] += tcnt[p];
-            tcnt[p] = 0;
-        }
-        __syncthreads();
     }
+}
+
+template <typename V>
+constexpr size_t seg_scatter_smem() {
+    return (size_t)SEG_TILE * (sizeof(V) + 4 + 1) + 4 * (size_t)SEG_NW * SEG_FMAX + 8 * (size_t)SEG_FMAX +
+           8 * (size_t)SEG_FMAX + 4 * 32 + 64;
 }
 
 template <int DT, int K>
@@ -426,41 +670,55 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
                     int *launches) {
     using V = typename Fmt<DT>::V;
     if (n >= ((int64_t)1 << 32)) return -1;  // 32-bit partition cursors (callers split larger inputs)
-    const Plan pl = make_plan(n, G);
+    const Plan pl = make_plan(n, G, DT);
     PartWs w = carve(ws, n, G, K, DT, pl);
     if (w.bytes > ws_bytes) return -1;
-    const size_t hsm = 4 * (size_t)pl.P, ssm = ScatterSmem<V>::bytes(pl.P);
-    if (hsm > (size_t)device_props().smem_optin) return -1;
-    if (n > 0) {
-        cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-        int tk = trace_begin(st);
-        k_part_hist<<<pl.B, HIST_TPB, hsm, st>>>(keys, n, G, pl.P, pl.chunk, w.hist, status);
-        trace_end(tk, "part_hist", st);
-        ++*launches;
-        tk = trace_begin(st);
-        k_part_colscan<<<(pl.P + 255) / 256, 256, 0, st>>>(w.hist, pl.B, pl.P, w.ptot);
-        trace_end(tk, "part_colscan", st);
+    constexpr size_t ssm = seg_scatter_smem<V>();
+    if (ssm > (size_t)device_props().smem_optin) return -1;
+    if (n == 0) {
+        cudaMemsetAsync(w.ptot, 0, 8 * (size_t)pl.Pf, st);
+        int tp = trace_begin(st);
+        k_part_plan<<<1, 1024, 0, st>>>(w.ptot, pl.Pf, pl.ch, w.base, w.pitem, w.items, w.iown, w.ctrl);
+        trace_end(tp, "part_plan", st);
         ++*launches;
     } else {
-        cudaMemsetAsync(w.ptot, 0, 8 * (size_t)pl.P, st);
-    }
-    int tp = trace_begin(st);
-    k_part_plan<<<1, 1024, 0, st>>>(w.ptot, pl.P, pl.ch, w.base, w.pitem, w.items, w.iown, w.ctrl);
-    trace_end(tp, "part_plan", st);
-    ++*launches;
-    if (n > 0) {
-        int ts = trace_begin(st);
-        if (pl.P > 8 && pl.P <= 4096) {
-            cudaFuncSetAttribute(k_part_scatter<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
-            k_part_scatter<V><<<pl.B, SC_TPB, ssm, st>>>(keys, (const V *)vals, n, G, pl.P, pl.chunk, w.hist,
-                                                         w.base, w.pkeys, (V *)w.pvals);
-        } else {
-            cudaFuncSetAttribute(k_part_scatter_direct<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-            k_part_scatter_direct<V><<<pl.B, HIST_TPB, hsm, st>>>(keys, (const V *)vals, n, G, pl.P, pl.chunk,
-                                                                  w.hist, w.base, w.pkeys, (V *)w.pvals);
+        cudaFuncSetAttribute(k_seg_scatter<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+        const int32_t *ik = keys;
+        const V *iv = (const V *)vals;
+        int S = 1;
+        for (int pass = 0; pass < pl.passes; ++pass) {
+            const bool last = pass + 1 == pl.passes;
+            const int bits = pl.bits[pass], F = 1 << bits;
+            int32_t *ok = last ? w.pkeys : w.akeys;
+            V *ov = (V *)(last ? w.pvals : w.avals);
+            int tk = trace_begin(st);
+            k_seg_units<<<1, 1024, 0, st>>>(pass == 0 ? nullptr : w.base, S, n, pl.cu, w.units, w.useg, w.ufirst);
+            ++*launches;
+            k_seg_hist<<<pl.grid, SEG_TPB, 0, st>>>(ik, w.units, w.ufirst, S, pl.shift[pass], bits, G, pass == 0,
+                                                     w.hist, status);
+            ++*launches;
+            k_seg_scan<<<S * F, 256, 0, st>>>(w.hist, w.ufirst, bits, w.ptot);
+            ++*launches;
+            k_part_plan<<<1, 1024, 0, st>>>(w.ptot, S * F, pl.ch, w.base, w.pitem, w.items, w.iown, w.ctrl);
+            ++*launches;
+            trace_end(tk, "part_hist", st);
+            tk = trace_begin(st);
+            if (bits <= SEG_MAX_BITS) {
+                k_seg_scatter<V><<<pl.grid, SEG_TPB, ssm, st>>>(ik, iv, w.units, w.useg, w.ufirst, S, pl.shift[pass],
+                                                               bits, G, last ? 1 : 0, w.hist, w.base, ok, ov);
+            } else {
+                const size_t wsm = seg_scatter_wide_smem<V>(F);
+                cudaFuncSetAttribute(k_seg_scatter_wide<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
+                k_seg_scatter_wide<V><<<pl.grid, WS_TPB, wsm, st>>>(ik, iv, w.units, w.useg, w.ufirst, S,
+                                                                    pl.shift[pass], bits, G, last ? 1 : 0, w.hist,
+                                                                    w.base, ok, ov);
+            }
+            trace_end(tk, "part_scatter", st);
+            ++*launches;
+            ik = ok;
+            iv = ov;
+            S *= F;
         }
-        trace_end(ts, "part_scatter", st);
-        ++*launches;
         // per-partition tables: Gp = 1024 groups, level sums in registers
         auto kern = k_part_accumulate<DT, K>;
         const size_t smem = onchip_smem_bytes<DT, K>(PART_GP, true);
@@ -487,15 +745,11 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
 
 }  // namespace
 
-// one partitioning pass: histogram and direct scatter keep one 32-bit counter
-// per partition in shared memory
-int partition_max_groups(int, int) {
-    const int64_t parts = (int64_t)device_props().smem_optin / 4;
-    return (int)std::min<int64_t>(parts * PART_GP, (int64_t)1 << 30);
-}
+// at most two passes of <= 2^8 digits: 2^16 partitions of 1024 groups
+int partition_max_groups(int, int) { return 1 << (2 * SEG_MAX_BITS + PART_LOG_GP); }
 
 size_t partition_workspace_bytes(int64_t n, int32_t G, int K, int DT) {
-    const Plan pl = make_plan(n, G);
+    const Plan pl = make_plan(n, G, DT);
     return carve(nullptr, n, G, K, DT, pl).bytes;
 }
 

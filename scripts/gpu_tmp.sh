@@ -1,6 +1,8 @@
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_synth.py -q 2>&1 | tail -2
-timeout 900 python bench.py --config 4 --steps 10 --warmup 3 > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.err; echo "rc=$?"; tail -3 gpurun_out/bench_c4.err
-timeout 900 python bench.py --steps 100 --warmup 5 > gpurun_out/bench_c1.json 2> gpurun_out/bench_c1.err; echo "rc=$?"; tail -3 gpurun_out/bench_c1.err
-cat gpurun_out/bench_c4.json gpurun_out/bench_c1.json
+for v in o64_7 o64_8 o64_10; do
+  echo "== $v"
+  export REPRO_B200_LIB=$PWD/scripts/variants/lib_$v.so
+  for G in 262144 1048576; do
+    timeout 600 python bench.py --config 2 --n-groups $G --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-atomic-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($G, round(d['ms_per_step'],3), {k:round(v,3) for k,v in d['per_kernel_ms'].items()})"
+  done
+done
