@@ -397,13 +397,16 @@ __device__ __forceinline__ int check_row(int key, typename Fmt<DT>::V v, bool in
 // accumulate_range reads, per input row, one int32 key and NCOL value columns
 // and turns them into NV virtual rows (virtual key, value); every virtual row
 // is deposited like a row of a single-column GroupBy over the virtual groups.
-// R = input rows per thread per tile.
+// R = input rows per thread per tile.  ONES: the last virtual column is the
+// constant 1 (COUNT); the fast path deposits its digits -- the same for every
+// row under a block-uniform window -- without a digit cascade per row.
 
 // plain GroupBy-SUM of one column
 template <int DT>
 struct SrcSingle {
     using V = typename Fmt<DT>::V;
     static constexpr int NCOL = 1, NV = 1;
+    static constexpr bool ONES = false;  // last virtual column constant 1 (COUNT)
     static constexpr int R = (DT == 1) ? ONCHIP_R64 : ONCHIP_R32;
     const V *col[NCOL];
     int G;
@@ -421,6 +424,7 @@ template <int DT, int NC>
 struct SrcCols {
     using V = typename Fmt<DT>::V;
     static constexpr int NCOL = NC, NV = NC + 1;
+    static constexpr bool ONES = true;
     static constexpr int R = ONCHIP_RMULTI;
     const V *col[NCOL];
     int G;
@@ -441,6 +445,7 @@ struct SrcCols {
 struct SrcQ1 {
     using V = double;
     static constexpr int NCOL = 4, NV = 5;
+    static constexpr bool ONES = true;
     static constexpr int R = ONCHIP_RMULTI;
     const double *col[NCOL];
     int G;
@@ -484,9 +489,12 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
     constexpr int NCOL = SRC::NCOL, NV = SRC::NV;
     constexpr int TPB = Cfg::TPB, RIN = SRC::R, TILE = TPB * RIN, CW = Cfg::CW;
     constexpr int R = RIN * NV;            // virtual rows per thread per tile
-    constexpr int VTILE = TILE * NV;       // virtual rows per tile (fold accounting)
+    // fold accounting: a counter of a virtual group receives at most one limb
+    // per INPUT row (virtual group j * G + g only gets column j of rows with
+    // key g), so the limb headroom is counted in input rows
+    constexpr int VTILE = TILE;
     constexpr size_t ROWB = 4 + NCOL * sizeof(V);  // bytes per input row in a ring stage
-    static_assert(VTILE <= Cfg::LIMIT, "tile larger than limb headroom");
+    static_assert(TILE <= Cfg::LIMIT, "tile larger than limb headroom");
     const int gq = onchip_gq<DT, K>(G, REGTOT);
     const int nq = gq >> 2;  // group quads
 
@@ -587,9 +595,9 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         V vv[NV];
         src.expand(k, c, vk, vv);
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            key[i * NV + j] = in ? vk[j] : -1;
-            val[i * NV + j] = in ? vv[j] : V(0);
+        for (int j = 0; j < NV; ++j) {  // column-major: virtual row j * RIN + i
+            key[j * RIN + i] = in ? vk[j] : -1;
+            val[j * RIN + i] = in ? vv[j] : V(0);
         }
     };
     auto load_tile = [&](int64_t b, int32_t(&key)[R], V(&val)[R]) {
@@ -694,13 +702,32 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                 }
                 since += VTILE;
                 const Extractors<DT, K> ex(kuni);
-                constexpr int NB = ONCHIP_NB < R ? ONCHIP_NB : R;
+                constexpr int RD = SRC::ONES ? R - RIN : R;  // virtual rows with a digit cascade
+                constexpr int NB = ONCHIP_NB < RD ? ONCHIP_NB : RD;
 #pragma unroll
-                for (int i0 = 0; i0 < R; i0 += NB) {
-                    if (i0 + NB <= R) deposit_batch<DT, K, NB>(fbase, kstride, wstride, key + i0, val + i0, ex);
+                for (int i0 = 0; i0 < RD; i0 += NB) {
+                    if (i0 + NB <= RD) deposit_batch<DT, K, NB>(fbase, kstride, wstride, key + i0, val + i0, ex);
                     else
-                        deposit_batch<DT, K, (R % NB ? R % NB : NB)>(fbase, kstride, wstride, key + i0, val + i0,
-                                                                     ex);
+                        deposit_batch<DT, K, (RD % NB ? RD % NB : NB)>(fbase, kstride, wstride, key + i0, val + i0,
+                                                                       ex);
+                }
+                if (SRC::ONES) {
+                    // COUNT column: the limbs of 1 under the window kuni, once per tile
+                    uint32_t clo[K], chi[K];
+                    row_limbs<DT, K>(F::pow2(F::m - F::W * kuni), clo, chi);
+#pragma unroll
+                    for (int l = 0; l < K; ++l) {
+#pragma unroll
+                        for (int h = 0; h < Cfg::LIMBS; ++h) {
+                            const uint32_t c = h ? chi[l] : clo[l];
+                            if (c != 0u) {
+                                const uint32_t off = (uint32_t)(Cfg::LIMBS * l + h) * wstride;
+#pragma unroll
+                                for (int i = 0; i < RIN; ++i)  // fast path: every key is valid
+                                    red_shared(fbase + kstride * (uint32_t)key[R - RIN + i] + off, c);
+                            }
+                        }
+                    }
                 }
                 continue;
             }
@@ -711,7 +738,7 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 int ks;
-                const int k = check_row<DT>(key[i], val[i], (i / NV) * TPB < rem, G, flags, ks);
+                const int k = check_row<DT>(key[i], val[i], (i % RIN) * TPB < rem, G, flags, ks);
                 if (k >= 0 && ks > kuni) { atomicMax(&ktop_next[k], ks); changed = 1; }
                 key[i] = k;
                 kc[i] = kuni;
@@ -720,7 +747,7 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
 #pragma unroll
             for (int i = 0; i < R; ++i) {
                 int ks;
-                const int k = check_row<DT>(key[i], val[i], (i / NV) * TPB < rem, G, flags, ks);
+                const int k = check_row<DT>(key[i], val[i], (i % RIN) * TPB < rem, G, flags, ks);
                 const int cur = k >= 0 ? ktop_cur[k] : 0;
                 if (k >= 0 && ks > cur) { atomicMax(&ktop_next[k], ks); changed = 1; }
                 key[i] = k;
