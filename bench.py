@@ -398,8 +398,19 @@ def main():
         for _ in range(e2e_steps):
             res = R.groupby_sum_host(kp, vp, G, K)
         et = (time.perf_counter() - t0) / e2e_steps
+        # the PCIe ceiling for context: the same bytes, plain pinned H2D copies
+        kd2, vd2 = torch.empty_like(keys), torch.empty_like(cols[0])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            kd2.copy_(kp, non_blocking=True)
+            vd2.copy_(vp, non_blocking=True)
+        torch.cuda.synchronize()
+        h2d = 3 * n * row_bytes / (time.perf_counter() - t0) / 1e9
+        del kd2, vd2
         line["e2e"] = {"value": n / et, "unit": "rows/s", "h2d_bytes_per_step": n * row_bytes,
                        "d2h_bytes_per_step": G * vsz, "ms_per_step": et * 1e3, "steps": e2e_steps,
+                       "h2d_copy_gbs": h2d, "e2e_gbs": n * row_bytes / et / 1e9,
                        "bit_identical_to_device_path": bool(torch.equal(res, out.cpu()))}
         del kp, vp
 

@@ -166,6 +166,68 @@ struct Cache {
     int device = -1;
 } g_cache;
 
+// Device buffers, streams and events of repro_groupby_sum_host, kept across
+// calls (allocating ~0.2 GB and creating streams per call cost milliseconds).
+struct HostCtx {
+    static constexpr int NB = 3;
+    std::mutex mu;
+    int device = -1;
+    cudaStream_t cs = nullptr, ks = nullptr;
+    cudaEvent_t copied[NB] = {}, consumed[NB] = {};
+    void *dbuf = nullptr, *dout = nullptr, *ws = nullptr, *pin = nullptr;
+    size_t dbuf_b = 0, dout_b = 0, ws_b = 0, pin_b = 0;
+
+    static int grow(void **p, size_t *have, size_t want, bool host) {
+        if (*have >= want && *p) return REPRO_OK;
+        if (*p) host ? cudaFreeHost(*p) : cudaFree(*p);
+        *p = nullptr;
+        *have = 0;
+        if (want == 0) return REPRO_OK;
+        if ((host ? cudaMallocHost(p, want) : cudaMalloc(p, want)) != cudaSuccess) {
+            cudaGetLastError();
+            *p = nullptr;
+            return REPRO_ENOMEM;
+        }
+        *have = want;
+        return REPRO_OK;
+    }
+    int prepare(size_t dbuf_want, size_t dout_want, size_t ws_want, size_t pin_want) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (device != dev) {  // (re)create per device; buffers of another device are dropped
+            if (cs) cudaStreamDestroy(cs);
+            if (ks) cudaStreamDestroy(ks);
+            for (int b = 0; b < NB; ++b) {
+                if (copied[b]) cudaEventDestroy(copied[b]);
+                if (consumed[b]) cudaEventDestroy(consumed[b]);
+            }
+            dbuf = dout = ws = nullptr;
+            dbuf_b = dout_b = ws_b = 0;
+            if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess ||
+                cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking) != cudaSuccess)
+                return REPRO_ECUDA;
+            for (int b = 0; b < NB; ++b)
+                if (cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&consumed[b], cudaEventDisableTiming) != cudaSuccess)
+                    return REPRO_ECUDA;
+            device = dev;
+        }
+        int st = grow(&dbuf, &dbuf_b, dbuf_want, false);
+        if (st == REPRO_OK) st = grow(&dout, &dout_b, std::max<size_t>(dout_want, 8), false);
+        if (st == REPRO_OK) st = grow(&ws, &ws_b, std::max<size_t>(ws_want, ALIGN), false);
+        if (st == REPRO_OK && pin_want) st = grow(&pin, &pin_b, pin_want, true);
+        return st;
+    }
+    void release() {
+        if (dbuf) cudaFree(dbuf);
+        if (dout) cudaFree(dout);
+        if (ws) cudaFree(ws);
+        if (pin) cudaFreeHost(pin);
+        dbuf = dout = ws = pin = nullptr;
+        dbuf_b = dout_b = ws_b = pin_b = 0;
+    }
+} g_host;
+
 void *cache_get(size_t bytes) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -505,6 +567,10 @@ int repro_synth_generate(int32_t config, uint64_t seed, int64_t r0, int64_t n, i
 }
 
 void repro_release_cache(void) {
+    {
+        std::lock_guard<std::mutex> lock(g_host.mu);
+        g_host.release();
+    }
     std::lock_guard<std::mutex> lock(g_cache.mu);
     if (g_cache.ptr) cudaFree(g_cache.ptr);
     g_cache.ptr = nullptr;
@@ -522,11 +588,6 @@ int repro_groupby_sum_host(const int32_t *keys_host, const void *vals_host, int6
     const size_t vsz = dtype == REPRO_F64 ? 8 : 4;
     const int path = choose_path(n_groups, fold, dtype);
     if (path < 0) return REPRO_EINVAL;
-    int status = REPRO_OK;
-    cudaStream_t cs = nullptr, ks = nullptr;
-    cudaEvent_t copied[2] = {}, consumed[2] = {};
-    void *dbuf = nullptr, *dout = nullptr, *ws = nullptr;
-    void *pin[2] = {};
     bool pinned_input = false;
     {
         cudaPointerAttributes a{};
@@ -536,9 +597,19 @@ int repro_groupby_sum_host(const int32_t *keys_host, const void *vals_host, int6
         }
         cudaGetLastError();
     }
+    // on-chip path: chunks of CH rows through NB device buffers; the copy
+    // stream waits on the kernel stream only through events (no host sync
+    // when the input is pinned), so H2D streams back to back
     const int64_t CH = path == 0 ? ((int64_t)1 << 23) : std::max<int64_t>(n, 1);
-    const int nb = path == 0 ? 2 : 1;
-    const size_t chunk_bytes = (size_t)std::min<int64_t>(CH, std::max<int64_t>(n, 1)) * (4 + vsz);
+    const int nb = path == 0 ? HostCtx::NB : 1;
+    const size_t chunk_bytes = align_up((size_t)std::min<int64_t>(CH, std::max<int64_t>(n, 1)) * 4) +
+                               (size_t)std::min<int64_t>(CH, std::max<int64_t>(n, 1)) * vsz;
+    const size_t need = ws_bytes_for(path, n, n_groups, fold, dtype);
+    std::lock_guard<std::mutex> lock(g_host.mu);
+    HostCtx &h = g_host;
+    int status = h.prepare(chunk_bytes * nb + ALIGN, vsz * (size_t)n_groups, need,
+                           pinned_input ? 0 : chunk_bytes);
+    if (status != REPRO_OK) return status;
 #define CK(x)                                    \
     do {                                         \
         if ((x) != cudaSuccess) {                \
@@ -546,82 +617,60 @@ int repro_groupby_sum_host(const int32_t *keys_host, const void *vals_host, int6
             goto done;                           \
         }                                        \
     } while (0)
-    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&ks, cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b) {
-        CK(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
-        CK(cudaEventCreateWithFlags(&consumed[b], cudaEventDisableTiming));
-    }
-    CK(cudaMalloc(&dbuf, chunk_bytes * nb + ALIGN));
-    CK(cudaMalloc(&dout, vsz * (size_t)n_groups));
-    {
-        const size_t need = ws_bytes_for(path, n, n_groups, fold, dtype);
-        CK(cudaMalloc(&ws, need));
-        if (!pinned_input)
-            for (int b = 0; b < nb; ++b) CK(cudaMallocHost(&pin[b], chunk_bytes));
-        if (path == 0) {
-            OnchipWs w = carve_onchip(ws, n, n_groups, fold, dtype);
-            CK(cudaMemsetAsync(ws, 0, w.zero_bytes, ks));
-            int c = 0;
-            for (int64_t r0 = 0; r0 < n; r0 += CH, ++c) {
-                const int b = c % nb;
-                const int64_t rows = std::min<int64_t>(CH, n - r0);
-                char *dk = (char *)dbuf + (size_t)b * chunk_bytes;
-                char *dv = dk + align_up((size_t)rows * 4);
-                if (c >= nb) CK(cudaEventSynchronize(consumed[b]));  // host staging + device buffer free
-                const char *hk = (const char *)keys_host + (size_t)r0 * 4;
-                const char *hv = (const char *)vals_host + (size_t)r0 * vsz;
-                if (!pinned_input) {
-                    memcpy(pin[b], hk, (size_t)rows * 4);
-                    memcpy((char *)pin[b] + align_up((size_t)rows * 4), hv, (size_t)rows * vsz);
-                    hk = (const char *)pin[b];
-                    hv = (const char *)pin[b] + align_up((size_t)rows * 4);
-                }
-                CK(cudaMemcpyAsync(dk, hk, (size_t)rows * 4, cudaMemcpyHostToDevice, cs));
-                CK(cudaMemcpyAsync(dv, hv, (size_t)rows * vsz, cudaMemcpyHostToDevice, cs));
-                CK(cudaEventRecord(copied[b], cs));
-                CK(cudaStreamWaitEvent(ks, copied[b], 0));
-                int rc = timed("onchip_accumulate", ks, [&] {
-                    return launch_onchip_any(dtype, fold, (const int32_t *)dk, dv, rows, n_groups, w.kglob,
-                                             w.slots, w.flags, ks, &t_launches);
-                });
-                if (rc) { status = map_launch(rc); goto done; }
-                CK(cudaEventRecord(consumed[b], ks));
+    if (path == 0) {
+        OnchipWs w = carve_onchip(h.ws, n, n_groups, fold, dtype);
+        CK(cudaMemsetAsync(h.ws, 0, w.zero_bytes, h.ks));
+        int c = 0;
+        for (int64_t r0 = 0; r0 < n; r0 += CH, ++c) {
+            const int b = c % nb;
+            const int64_t rows = std::min<int64_t>(CH, n - r0);
+            char *dk = (char *)h.dbuf + (size_t)b * chunk_bytes;
+            char *dv = dk + align_up((size_t)rows * 4);
+            const char *hk = (const char *)keys_host + (size_t)r0 * 4;
+            const char *hv = (const char *)vals_host + (size_t)r0 * vsz;
+            if (c >= nb) CK(cudaStreamWaitEvent(h.cs, h.consumed[b], 0));  // device buffer b is free
+            if (!pinned_input) {
+                // pageable input: stage through one pinned buffer (host waits for its copy)
+                CK(cudaStreamSynchronize(h.cs));
+                memcpy(h.pin, hk, (size_t)rows * 4);
+                memcpy((char *)h.pin + align_up((size_t)rows * 4), hv, (size_t)rows * vsz);
+                hk = (const char *)h.pin;
+                hv = (const char *)h.pin + align_up((size_t)rows * 4);
             }
-            int rc = timed("fold", ks, [&] {
-                return launch_fold(dtype, fold, n_groups, w.kglob, w.slots, 0, nullptr, nullptr, nullptr, dout,
-                                   w.flags, ks, &t_launches);
+            CK(cudaMemcpyAsync(dk, hk, (size_t)rows * 4, cudaMemcpyHostToDevice, h.cs));
+            CK(cudaMemcpyAsync(dv, hv, (size_t)rows * vsz, cudaMemcpyHostToDevice, h.cs));
+            CK(cudaEventRecord(h.copied[b], h.cs));
+            CK(cudaStreamWaitEvent(h.ks, h.copied[b], 0));
+            int rc = timed("onchip_accumulate", h.ks, [&] {
+                return launch_onchip_any(dtype, fold, (const int32_t *)dk, dv, rows, n_groups, w.kglob, w.slots,
+                                         w.flags, h.ks, &t_launches);
             });
             if (rc) { status = map_launch(rc); goto done; }
-            CK(cudaMemcpyAsync(out_host, dout, vsz * (size_t)n_groups, cudaMemcpyDeviceToHost, ks));
-            status = finish_blocking(w.flags, ks);
-        } else {
-            char *dk = (char *)dbuf;
-            char *dv = dk + align_up((size_t)n * 4);
-            CK(cudaMemcpyAsync(dk, keys_host, (size_t)n * 4, cudaMemcpyHostToDevice, ks));
-            CK(cudaMemcpyAsync(dv, vals_host, (size_t)n * vsz, cudaMemcpyHostToDevice, ks));
-            uint32_t *flags = nullptr;
-            int rc = enqueue_groupby((const int32_t *)dk, dv, n, n_groups, fold, dtype, dout, 0, nullptr, nullptr,
-                                     nullptr, ws, need, ks, &flags);
-            if (rc != REPRO_OK) { status = rc; goto done; }
-            CK(cudaMemcpyAsync(out_host, dout, vsz * (size_t)n_groups, cudaMemcpyDeviceToHost, ks));
-            status = finish_blocking(flags, ks);
+            CK(cudaEventRecord(h.consumed[b], h.ks));
         }
+        int rc = timed("fold", h.ks, [&] {
+            return launch_fold(dtype, fold, n_groups, w.kglob, w.slots, 0, nullptr, nullptr, nullptr, h.dout, w.flags,
+                               h.ks, &t_launches);
+        });
+        if (rc) { status = map_launch(rc); goto done; }
+        CK(cudaMemcpyAsync(out_host, h.dout, vsz * (size_t)n_groups, cudaMemcpyDeviceToHost, h.ks));
+        status = finish_blocking(w.flags, h.ks);
+    } else {
+        char *dk = (char *)h.dbuf;
+        char *dv = dk + align_up((size_t)n * 4);
+        CK(cudaMemcpyAsync(dk, keys_host, (size_t)n * 4, cudaMemcpyHostToDevice, h.ks));
+        CK(cudaMemcpyAsync(dv, vals_host, (size_t)n * vsz, cudaMemcpyHostToDevice, h.ks));
+        uint32_t *flags = nullptr;
+        int rc = enqueue_groupby((const int32_t *)dk, dv, n, n_groups, fold, dtype, h.dout, 0, nullptr, nullptr,
+                                 nullptr, h.ws, need, h.ks, &flags);
+        if (rc != REPRO_OK) { status = rc; goto done; }
+        CK(cudaMemcpyAsync(out_host, h.dout, vsz * (size_t)n_groups, cudaMemcpyDeviceToHost, h.ks));
+        status = finish_blocking(flags, h.ks);
     }
 done:
 #undef CK
-    if (ks) cudaStreamSynchronize(ks);
-    if (cs) cudaStreamSynchronize(cs);
-    for (int b = 0; b < 2; ++b) {
-        if (pin[b]) cudaFreeHost(pin[b]);
-        if (copied[b]) cudaEventDestroy(copied[b]);
-        if (consumed[b]) cudaEventDestroy(consumed[b]);
-    }
-    if (dbuf) cudaFree(dbuf);
-    if (dout) cudaFree(dout);
-    if (ws) cudaFree(ws);
-    if (cs) cudaStreamDestroy(cs);
-    if (ks) cudaStreamDestroy(ks);
+    cudaStreamSynchronize(h.ks);
+    cudaStreamSynchronize(h.cs);
     return status;
 }
 
