@@ -12,7 +12,7 @@ Workload at N=1 (default): BASELINE.json configs[1] (2^27 rows, int32 keys
 U[0,1024), fp64 values +-(1+mant) 2^e, e in [-20,20], fold K=3), the config
 the metric is quoted on.  At N>1 every rank processes its own shard of the
 same generator (weak scaling: each rank its own 2^27 rows) and the states are
-combined with integer all-reduces.  `--config 2 --n-groups G`, `--config 3`
+combined with integer all-reduces (config 4: of the fused pass's slot tables).  `--config 2 --n-groups G`, `--config 3`
 and `--config 4` time the other BASELINE configs (parity/sweep runs; config 4
 is the multi-column call: 4 reproducible SUMs + COUNT over a row projection).
 
@@ -269,8 +269,6 @@ def main():
     dt = R.F64 if dts == "f64" else R.F32
     vsz = 8 if dt == R.F64 else 4
     multi = args.config == 4
-    if multi and world > 1:
-        raise SystemExit("config 4 (multi-column) runs on one GPU in this build; see DESIGN.md 'Multi-GPU'")
     ncol = 4 if multi else 1
     row_bytes = 4 + ncol * vsz
     keys, cols = device_rows(R, torch, args.config, rank * n, n, G)
@@ -290,7 +288,10 @@ def main():
 
     def step():
         if multi:
-            R.groupby_sum_multi_async(keys, cols, G, K, 1, outs, counts, ws, status, stream)
+            if world == 1:
+                R.groupby_sum_multi_async(keys, cols, G, K, 1, outs, counts, ws, status, stream)
+            else:  # deposit, all-reduce the integer slot tables, read out on every rank
+                rdist.groupby_sum_multi_dist(R, keys, cols, G, K, 1, outs, counts, ws, status, stream=stream)
             return
         if world == 1:
             R.groupby_sum_async(keys, cols[0], G, K, out, ws, status, stream)

@@ -99,6 +99,32 @@ int repro_groupby_sum_host(const int32_t *keys_host, const void *vals_host,
 /* Free the internal workspace cache of the blocking entry points. */
 void repro_release_cache(void);
 
+/* Split form of the fused multi-column call for several GPUs (SURVEY.md
+ * 8(e)); only for shapes the fused pass covers (n_groups * (outputs + 1) <=
+ * 1024), else REPRO_EINVAL.  Each rank deposits its rows into the absolute-
+ * level slot table inside its workspace (same workspace size as
+ * repro_groupby_sum_multi_async), the caller all-reduces that table across
+ * the ranks -- the status word with bitwise OR, kglob (int32) with MAX, slots
+ * (uint64, used as int64) with SUM: integer operations, so the result does not
+ * depend on the reduction order -- and every rank finishes: Eq. 1 read-out of
+ * the summed table, scatter to outs / counts, device status word.
+ * repro_groupby_multi_table gives the byte offsets inside the workspace and
+ * the element counts of [flags (uint32), kglob (int32), slots (uint64)]. */
+int repro_groupby_multi_table(int64_t n, int32_t n_groups, int32_t ncols,
+                              int32_t proj, int32_t fold, int32_t dtype,
+                              int64_t *offsets, int64_t *counts);
+int repro_groupby_multi_deposit_async(const int32_t *keys,
+                                      const void *const *cols, int32_t ncols,
+                                      int32_t proj, int64_t n, int32_t n_groups,
+                                      int32_t fold, int32_t dtype,
+                                      void *workspace, size_t ws_bytes,
+                                      void *stream);
+int repro_groupby_multi_finish_async(int64_t n, int32_t n_groups, int32_t ncols,
+                                     int32_t proj, int32_t fold, int32_t dtype,
+                                     void *const *outs, int64_t *counts,
+                                     void *workspace, size_t ws_bytes,
+                                     void *stream, int32_t *d_status);
+
 /* Bench / test support, not part of the method: the seeded synthetic input
  * generator of paper_1802_09883_b200/synth.py run on the device (rows r0 ..
  * r0+n of BASELINE config 0/1/2 -- one binary64 column -- or 4 -- columns

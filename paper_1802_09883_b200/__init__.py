@@ -51,6 +51,12 @@ _sig("repro_synth_generate", ctypes.c_int, _i32, ctypes.c_uint64, _i64, _i64, _i
 _sig("repro_groupby_sum_multi", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
      ctypes.POINTER(_vp), _vp)
 _sig("repro_groupby_multi_workspace_bytes", _sz, _i64, _i32, _i32, _i32, _i32, _i32)
+_sig("repro_groupby_multi_table", ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_i64),
+     ctypes.POINTER(_i64))
+_sig("repro_groupby_multi_deposit_async", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
+     _vp, _sz, _vp)
+_sig("repro_groupby_multi_finish_async", ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_vp), _vp,
+     _vp, _sz, _vp, _vp)
 _sig("repro_groupby_sum_multi_async", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
      ctypes.POINTER(_vp), _vp, _vp, _sz, _vp, _vp)
 _sig("repro_acc_create", ctypes.c_int, ctypes.POINTER(_vp), _i32, _i32, _i32)
@@ -258,6 +264,45 @@ def synth_generate(config: int, n: int, n_groups: int, r0: int = 0, seed: int | 
     _check(_lib.repro_synth_generate(config, seed, r0, n, n_groups, _dev(keys, "keys", torch.int32), cptr,
                                      _stream_ptr(stream)), "repro_synth_generate")
     return keys, cols
+
+
+def multi_table_views(workspace, n: int, n_groups: int, ncols: int, proj: int, fold: int, dtype: int):
+    """(flags int32[1], kglob int32[Gv], slots int64[...]) tensor views of the
+    slot table inside a multi-column workspace (make_multi_workspace)."""
+    torch = _torch()
+    off = (_i64 * 3)()
+    cnt = (_i64 * 3)()
+    _check(_lib.repro_groupby_multi_table(n, n_groups, ncols, proj, fold, dtype, off, cnt), "repro_groupby_multi_table")
+    base = _aligned_ptr(workspace)[0] - workspace.data_ptr()
+    views = []
+    for o, c, dt, sz in zip(off, cnt, (torch.int32, torch.int32, torch.int64), (4, 4, 8)):
+        views.append(workspace[base + o: base + o + c * sz].view(dt))
+    return tuple(views)
+
+
+def groupby_multi_deposit_async(keys, cols, n_groups: int, fold: int, proj: int, workspace, stream=None):
+    """Split form, step 1: deposit this rank's rows into the workspace's slot table."""
+    torch = _torch()
+    dt = _dtype_code(cols[0])
+    cptr = (_vp * len(cols))(*[_dev(c, "cols") for c in cols])
+    wp, wb = _aligned_ptr(workspace)
+    _check(_lib.repro_groupby_multi_deposit_async(_dev(keys, "keys", torch.int32), cptr, len(cols), proj,
+                                                  keys.numel(), n_groups, fold, dt, wp, wb, _stream_ptr(stream)),
+           "repro_groupby_multi_deposit_async")
+
+
+def groupby_multi_finish_async(n: int, n_groups: int, ncols: int, proj: int, fold: int, dtype: int, outs, counts,
+                               workspace, status, stream=None):
+    """Split form, step 3 (after the slot tables were all-reduced): read out."""
+    torch = _torch()
+    odt = torch.float64 if dtype == F64 else torch.float32
+    optr = (_vp * len(outs))(*[_dev(o, "outs", odt) for o in outs])
+    wp, wb = _aligned_ptr(workspace)
+    _check(_lib.repro_groupby_multi_finish_async(n, n_groups, ncols, proj, fold, dtype, optr,
+                                                 _dev(counts, "counts", torch.int64) if counts is not None else None,
+                                                 wp, wb, _stream_ptr(stream), _dev(status, "status", torch.int32)),
+           "repro_groupby_multi_finish_async")
+    return outs
 
 
 def baseline_atomic_sum(keys, vals, n_groups: int, variant: int = 0, accumulate_f64: bool = False, out=None,

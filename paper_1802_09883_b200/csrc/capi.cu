@@ -431,9 +431,11 @@ size_t multi_ws_bytes(int64_t n, int32_t G, int32_t ncols, int32_t proj, int32_t
     return ALIGN + (proj == 1 ? 2 * align_up(8 * (size_t)n) : 0) + ws_bytes_for(path, n, G, K, dt);
 }
 
+// phase: 3 = whole call; 1 = zero + deposit only (multi-GPU split form);
+// 2 = fold + scatter only (after the slot tables were all-reduced)
 int enqueue_multi(const int32_t *keys, const void *const *cols, int32_t ncols, int32_t proj, int64_t n, int32_t G,
                   int32_t K, int32_t dt, void *const *outs, int64_t *counts, void *ws, size_t ws_bytes,
-                  cudaStream_t st, uint32_t **flags_out) {
+                  cudaStream_t st, uint32_t **flags_out, int phase = 3) {
     if (ws_bytes < multi_ws_bytes(n, G, ncols, proj, K, dt)) return REPRO_ENOMEM;
     const int nout = multi_nout(proj, ncols);
     if (multi_fused(G, ncols, proj)) {
@@ -443,13 +445,16 @@ int enqueue_multi(const int32_t *keys, const void *const *cols, int32_t ncols, i
         OnchipWs w = carve_onchip(ws, n, Gv, K, dt);
         void *vout = (char *)ws + onchip_ws_bytes(n, Gv, K, dt);
         *flags_out = w.flags;
-        if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
-        int rc = timed("onchip_accumulate", st, [&] {
-            return launch_onchip_multi(dt, K, proj, ncols, keys, cols, n, G, w.kglob, w.slots, w.flags, st,
-                                       &t_launches);
-        });
-        if (rc) return map_launch(rc);
-        rc = timed("fold", st, [&] {
+        if (phase & 1) {
+            if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
+            int rc = timed("onchip_accumulate", st, [&] {
+                return launch_onchip_multi(dt, K, proj, ncols, keys, cols, n, G, w.kglob, w.slots, w.flags, st,
+                                           &t_launches);
+            });
+            if (rc) return map_launch(rc);
+        }
+        if (!(phase & 2)) return REPRO_OK;
+        int rc = timed("fold", st, [&] {
             return launch_fold(dt, K, Gv, w.kglob, w.slots, 0, nullptr, nullptr, nullptr, vout, w.flags, st,
                                &t_launches);
         });
@@ -514,6 +519,55 @@ bool multi_ptrs_ok(int64_t n, const int32_t *keys, const void *const *cols, int3
 }  // namespace
 
 extern "C" {
+
+int repro_groupby_multi_table(int64_t n, int32_t n_groups, int32_t ncols, int32_t proj, int32_t fold,
+                              int32_t dtype, int64_t *offsets, int64_t *counts) {
+    if (!multi_valid(n, n_groups, ncols, proj, fold, dtype) || !offsets || !counts) return REPRO_EINVAL;
+    if (!multi_fused(n_groups, ncols, proj)) return REPRO_EINVAL;
+    const int32_t Gv = n_groups * multi_virtual_columns(proj, ncols);
+    OnchipWs w = carve_onchip(nullptr, n, Gv, fold, dtype);
+    offsets[0] = (int64_t)(uintptr_t)w.flags;
+    offsets[1] = (int64_t)(uintptr_t)w.kglob;
+    offsets[2] = (int64_t)(uintptr_t)w.slots;
+    counts[0] = 1;
+    counts[1] = Gv;
+    counts[2] = (int64_t)Gv * slot_count(dtype, fold) * 2;
+    return REPRO_OK;
+}
+
+int repro_groupby_multi_deposit_async(const int32_t *keys, const void *const *cols, int32_t ncols, int32_t proj,
+                                      int64_t n, int32_t n_groups, int32_t fold, int32_t dtype, void *workspace,
+                                      size_t ws_bytes, void *stream) {
+    t_launches = 0;
+    if (!multi_valid(n, n_groups, ncols, proj, fold, dtype) || !workspace) return REPRO_EINVAL;
+    if (!multi_fused(n_groups, ncols, proj)) return REPRO_EINVAL;
+    if (n > 0 && (!keys || !cols)) return REPRO_EINVAL;
+    for (int c = 0; c < ncols && n > 0; ++c)
+        if (!cols[c]) return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    uint32_t *flags = nullptr;
+    return enqueue_multi(keys, cols, ncols, proj, n, n_groups, fold, dtype, nullptr, nullptr, workspace, ws_bytes,
+                         (cudaStream_t)stream, &flags, 1);
+}
+
+int repro_groupby_multi_finish_async(int64_t n, int32_t n_groups, int32_t ncols, int32_t proj, int32_t fold,
+                                     int32_t dtype, void *const *outs, int64_t *counts, void *workspace,
+                                     size_t ws_bytes, void *stream, int32_t *d_status) {
+    t_launches = 0;
+    if (!multi_valid(n, n_groups, ncols, proj, fold, dtype) || !workspace || !d_status) return REPRO_EINVAL;
+    if (!multi_fused(n_groups, ncols, proj)) return REPRO_EINVAL;
+    const int nout = multi_nout(proj, ncols);
+    if (!outs) return REPRO_EINVAL;
+    for (int c = 0; c < nout; ++c)
+        if (!outs[c]) return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *flags = nullptr;
+    int rc = enqueue_multi(nullptr, nullptr, ncols, proj, n, n_groups, fold, dtype, outs, counts, workspace, ws_bytes,
+                           st, &flags, 2);
+    if (rc != REPRO_OK) return rc;
+    return map_launch(timed("status", st, [&] { return launch_status(flags, d_status, st, &t_launches); }));
+}
 
 size_t repro_groupby_multi_workspace_bytes(int64_t n, int32_t n_groups, int32_t ncols, int32_t proj, int32_t fold,
                                            int32_t dtype) {

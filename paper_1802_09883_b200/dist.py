@@ -33,6 +33,32 @@ def allreduce_state(acc, group=None):
     return acc
 
 
+def allreduce_table(flags, kglob, slots, group=None):
+    """Combine the per-rank absolute-level slot tables of the fused
+    multi-column pass (repro_groupby_multi_table views): status bits OR-ed
+    (NCCL has no bitwise reduction: one MAX over the four bits), window tops
+    MAX, slot sums SUM -- integer operations, so every rank gets the same
+    table whatever the reduction order."""
+    bits = torch.stack([(flags[0] >> b) & 1 for b in range(4)]).to(torch.int32)
+    dist.all_reduce(bits, op=dist.ReduceOp.MAX, group=group)
+    flags.copy_((bits * torch.tensor([1, 2, 4, 8], dtype=torch.int32, device=bits.device)).sum().reshape(1))
+    dist.all_reduce(kglob, op=dist.ReduceOp.MAX, group=group)
+    dist.all_reduce(slots, op=dist.ReduceOp.SUM, group=group)
+
+
+def groupby_sum_multi_dist(R, keys, cols, n_groups, fold, proj, outs, counts, workspace, status, group=None,
+                           stream=None):
+    """Multi-column GroupBy over the rows of all ranks: deposit locally,
+    all-reduce the slot tables, read out on every rank."""
+    dt = R.F64 if cols[0].dtype == torch.float64 else R.F32
+    n = keys.numel()
+    R.groupby_multi_deposit_async(keys, cols, n_groups, fold, proj, workspace, stream)
+    flags, kglob, slots = R.multi_table_views(workspace, n, n_groups, len(cols), proj, fold, dt)
+    allreduce_table(flags, kglob, slots, group)
+    R.groupby_multi_finish_async(n, n_groups, len(cols), proj, fold, dt, outs, counts, workspace, status, stream)
+    return outs
+
+
 def shard_rows(n: int, world: int, rank: int):
     """Contiguous row range [r0, r1) of `rank` (rows are independent units)."""
     r0 = n * rank // world

@@ -128,3 +128,68 @@ def test_shard_rows_cover_everything():
             spans = [rdist.shard_rows(n, world, r) for r in range(world)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+# ---- slot-table exchange of the fused multi-column pass -------------------
+
+NS = {O.F64: 25, O.F32: 7}  # KMAX per dtype; a table row holds KMAX + K absolute-level slots
+
+
+def _slot_table(acc):
+    """The absolute-level slot table layout of the on-chip kernels (k_fold):
+    slots[g][level + K - 1] = (sum of low 32-bit parts, sum of high parts) of
+    the level sum at that absolute level, kglob[g] = window top."""
+    G, K = acc.G, acc.K
+    ns = NS[acc.dtype] + K
+    slots = np.zeros((G, ns, 2), np.int64)
+    for g in range(G):
+        k = int(acc.k[g])
+        for l in range(K):
+            T = acc.T[g][l]
+            slots[g, k - l + K - 1, 0] = T & 0xFFFFFFFF
+            slots[g, k - l + K - 1, 1] = T >> 32
+    return torch.tensor(acc.k, dtype=torch.int32), torch.from_numpy(slots.reshape(-1))
+
+
+def _table_worker(rank, world, port, keys, vals, G, K, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1802_09883_b200 import dist as rdist
+        r0, r1 = rdist.shard_rows(keys.size, world, rank)
+        acc = OracleAccumulator(keys[r0:r1], vals[r0:r1], G, K)
+        kglob, slots = _slot_table(acc)
+        flags = torch.tensor([1 << rank], dtype=torch.int32)  # each rank raises another status bit
+        rdist.allreduce_table(flags, kglob, slots)
+        # read the summed table under the global tops (what k_fold does)
+        ns = NS[acc.dtype] + K
+        S = slots.numpy().reshape(G, ns, 2)
+        acc.k = kglob.numpy().astype(np.int64)
+        acc.T = [[(int(S[g, int(acc.k[g]) - l + K - 1, 1]) << 32) + int(S[g, int(acc.k[g]) - l + K - 1, 0])
+                  for l in range(K)] for g in range(G)]
+        q.put((rank, int(flags.item()), acc.finalize().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_slot_table_exchange_equals_single_oracle():
+    rng = np.random.default_rng(21)
+    n, G, K = 5000, 9, 3
+    keys = rng.integers(0, G, n, dtype=np.int32)
+    vals = rng.uniform(-1, 1, n) * np.exp2(rng.integers(-60, 60, n))
+    vals[-5:] *= 2.0 ** 70  # only rank 1 sees the highest windows
+    rc, ref = O.groupby_sum(keys, vals, G, K)
+    assert rc == O.OK
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_table_worker, args=(r, 2, port, keys, vals, G, K, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {r: (f, b) for r, f, b in (q.get(timeout=120) for _ in range(2))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[0][0] == res[1][0] == 3  # status bits OR-ed
+    assert res[0][1] == res[1][1] == ref.tobytes()

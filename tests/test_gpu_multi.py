@@ -126,3 +126,31 @@ def test_multi_async_matches_blocking(R):
     for x, y in zip(outs, ref):
         assert torch.equal(x, y)
     assert torch.equal(counts, rc)
+
+
+def test_split_form_with_emulated_ranks(R):
+    # the multi-GPU split form on one GPU: two "ranks" deposit their halves into
+    # their own workspaces; their slot tables are combined the way
+    # dist.allreduce_table combines them (OR / MAX / SUM), then read out
+    keys, cols = synth.generate(4, n=300007)
+    kd, cd = dev(keys), [dev(c) for c in cols]
+    n, G, K = keys.size, 4, 3
+    h = n // 2
+    wss = [R.make_multi_workspace(n, G, 4, 1, K, R.F64) for _ in range(2)]
+    for w, (a, b) in zip(wss, ((0, h), (h, n))):
+        R.groupby_multi_deposit_async(kd[a:b], [c[a:b] for c in cd], G, K, 1, w)
+    t0 = R.multi_table_views(wss[0], n, G, 4, 1, K, R.F64)
+    t1 = R.multi_table_views(wss[1], n, G, 4, 1, K, R.F64)
+    t0[0].copy_(t0[0] | t1[0])
+    torch.maximum(t0[1], t1[1], out=t0[1])
+    t0[2].add_(t1[2])
+    outs = [torch.empty(G, dtype=torch.float64, device="cuda") for _ in range(4)]
+    counts = torch.empty(G, dtype=torch.int64, device="cuda")
+    st = torch.full((1,), 99, dtype=torch.int32, device="cuda")
+    R.groupby_multi_finish_async(n, G, 4, 1, K, R.F64, outs, counts, wss[0], st)
+    torch.cuda.synchronize()
+    assert st.item() == 0
+    ref, rc = R.groupby_sum_multi(kd, cd, G, K, proj=1)
+    for x, y in zip(outs, ref):
+        assert torch.equal(x, y)
+    assert torch.equal(counts, rc)
