@@ -146,13 +146,16 @@ int repro_synth_generate(int32_t config, uint64_t seed, int64_t r0, int64_t n,
  *   cols:  HOST array of ncols DEVICE pointers, each dtype[n].
  *   proj:  0 -- outs[c][g] = reproducible sum of cols[c] over group g
  *             (ncols in [1, 8], binary32 or binary64);
+ *          2 -- second moments (ncols == 1, column x): outs[0] = SUM(x),
+ *             outs[1] = SUM(x * x), each square rounded once;
  *          1 -- the config-4 projection (binary64 only, ncols == 4, columns
  *             qty, price, disc, tax): outs[0] = SUM(qty), outs[1] =
  *             SUM(price), outs[2] = SUM(price * (1 - disc)), outs[3] =
  *             SUM(price * (1 - disc) * (1 + tax)), every product and
  *             difference rounded separately to binary64 (no FMA; DESIGN.md
  *             reading A-15).
- *   outs:  HOST array of (proj ? 4 : ncols) DEVICE pointers, dtype[n_groups].
+ *   outs:  HOST array of (proj 1: 4, proj 2: 2, else ncols) DEVICE
+ *          pointers, dtype[n_groups].
  *   counts: DEVICE int64[n_groups] (exact row counts per group) or NULL.
  * Each SUM has the bits repro_groupby_sum would give on that column; rows
  * with a bad key raise REPRO_EKEY for the whole call.  One fused pass when
@@ -162,6 +165,20 @@ int repro_groupby_sum_multi(const int32_t *keys, const void *const *cols,
                             int32_t ncols, int32_t proj, int64_t n,
                             int32_t n_groups, int32_t fold, int32_t dtype,
                             void *const *outs, int64_t *counts);
+
+/* AVG / sample VARIANCE / STDDEV per group from reproducible SUMs (SURVEY.md
+ * 8(f) f2; the paper reduces every float aggregate to SUM):
+ * one fused pass computes SUM(x), SUM(x*x) and COUNT (proj 2 above), then,
+ * per group with c = COUNT, s = SUM(x), q = SUM(x*x), each operation rounded
+ * once in this order: avg = s / c; var = max(0, (q - (s * s) / c) / (c - 1))
+ * (0 when c <= 1); stddev = sqrt(var); an empty group gives avg = 0.  Every
+ * output is therefore exactly as reproducible as the SUMs.  sum, avg, var,
+ * stddev: DEVICE dtype[n_groups] (avg / var / stddev may be NULL); counts:
+ * DEVICE int64[n_groups] (required).  Blocking. */
+int repro_groupby_moments(const int32_t *keys, const void *vals, int64_t n,
+                          int32_t n_groups, int32_t fold, int32_t dtype,
+                          void *sum, void *avg, void *var, void *stddev,
+                          int64_t *counts);
 
 /* Workspace bytes of repro_groupby_sum_multi_async (0 on invalid shape). */
 size_t repro_groupby_multi_workspace_bytes(int64_t n, int32_t n_groups,

@@ -242,6 +242,9 @@ def groupby_sum_multi(keys: np.ndarray, cols, n_groups: int, fold: int, proj: in
         qty, price, disc, tax = cols
         dp, ch = q1_project(price, disc, tax)
         cols = [qty, price, dp, ch]
+    elif proj == 2:
+        x = np.ascontiguousarray(cols[0])
+        cols = [x, np.multiply(x, x)]  # one rounding per square
     outs, codes = [], []
     for c in cols:
         rc, o = groupby_sum(keys, np.ascontiguousarray(c), n_groups, fold, threads=threads)
@@ -251,3 +254,20 @@ def groupby_sum_multi(keys: np.ndarray, cols, n_groups: int, fold: int, proj: in
     ok = (keys >= 0) & (keys < n_groups)
     counts = np.bincount(keys[ok], minlength=n_groups).astype(np.int64)
     return status, outs, counts
+
+
+def groupby_moments(keys: np.ndarray, vals: np.ndarray, n_groups: int, fold: int, *, threads: int | None = None):
+    """Per-group SUM, AVG, sample VARIANCE, STDDEV, COUNT from the reproducible
+    SUM(x), SUM(x*x) and COUNT (groupby_sum_multi proj 2), with the formulas
+    of repro_groupby_moments evaluated in the value type, one rounding per
+    operation in the documented order (numpy elementwise ops)."""
+    rc, (s, q), c = groupby_sum_multi(keys, [vals], n_groups, fold, proj=2, threads=threads)
+    dt = vals.dtype.type
+    cf = c.astype(vals.dtype)
+    one, zero = dt(1), dt(0)
+    with np.errstate(divide="ignore", invalid="ignore"):
+        avg = np.where(c > 0, np.divide(s, cf), zero).astype(vals.dtype)
+        t = np.subtract(q, np.divide(np.multiply(s, s), cf))
+        var = np.where(c > 1, np.maximum(zero, np.divide(t, np.subtract(cf, one))), zero).astype(vals.dtype)
+    sd = np.sqrt(var).astype(vals.dtype)
+    return rc, {"sum": s, "avg": avg, "var": var, "stddev": sd, "count": c}

@@ -51,6 +51,7 @@ _sig("repro_synth_generate", ctypes.c_int, _i32, ctypes.c_uint64, _i64, _i64, _i
 _sig("repro_groupby_sum_multi", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
      ctypes.POINTER(_vp), _vp)
 _sig("repro_groupby_multi_workspace_bytes", _sz, _i64, _i32, _i32, _i32, _i32, _i32)
+_sig("repro_groupby_moments", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp)
 _sig("repro_groupby_multi_table", ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_i64),
      ctypes.POINTER(_i64))
 _sig("repro_groupby_multi_deposit_async", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
@@ -226,6 +227,21 @@ def groupby_sum_multi(keys, cols, n_groups: int, fold: int = 3, proj: int = 0, o
                                       optr, cnt)
     _check(st, "repro_groupby_sum_multi")
     return outs, (counts if with_counts else None)
+
+
+def groupby_moments(keys, vals, n_groups: int, fold: int = 3):
+    """Reproducible per-group SUM, AVG, sample VARIANCE, STDDEV and COUNT
+    (repro_groupby_moments).  Returns a dict of device tensors."""
+    torch = _torch()
+    dt = _dtype_code(vals)
+    if keys.numel() != vals.numel():
+        raise ValueError("keys and vals differ in length")
+    res = {k: torch.empty(n_groups, dtype=vals.dtype, device=vals.device) for k in ("sum", "avg", "var", "stddev")}
+    res["count"] = torch.empty(n_groups, dtype=torch.int64, device=vals.device)
+    _check(_lib.repro_groupby_moments(_dev(keys, "keys", torch.int32), _dev(vals, "vals"), keys.numel(), n_groups, fold,
+                                      dt, *[_dev(res[k], k, vals.dtype) for k in ("sum", "avg", "var", "stddev")],
+                                      _dev(res["count"], "count", torch.int64)), "repro_groupby_moments")
+    return res
 
 
 def multi_workspace_bytes(n: int, n_groups: int, ncols: int, proj: int, fold: int, dtype: int) -> int:

@@ -403,11 +403,12 @@ int repro_groupby_sum(const int32_t *keys, const void *vals, int64_t n, int32_t 
 
 namespace {
 
-int multi_nout(int32_t proj, int32_t ncols) { return proj == 1 ? 4 : ncols; }
+int multi_nout(int32_t proj, int32_t ncols) { return proj == 1 ? 4 : proj == 2 ? 2 : ncols; }
 
 bool multi_valid(int64_t n, int32_t G, int32_t ncols, int32_t proj, int32_t K, int32_t dt) {
     if (n < 0 || !valid_shape(G, K, dt)) return false;
     if (proj == 1) return ncols == 4 && dt == REPRO_F64;
+    if (proj == 2) return ncols == 1;
     return proj == 0 && ncols >= 1 && ncols <= 8;
 }
 
@@ -428,7 +429,9 @@ size_t multi_ws_bytes(int64_t n, int32_t G, int32_t ncols, int32_t proj, int32_t
     }
     const int path = choose_path(G, K, dt);
     if (path < 0) return 0;
-    return ALIGN + (proj == 1 ? 2 * align_up(8 * (size_t)n) : 0) + ws_bytes_for(path, n, G, K, dt);
+    const size_t vsz_ = dt == REPRO_F64 ? 8 : 4;
+    const size_t proj_bytes = proj == 1 ? 2 * align_up(8 * (size_t)n) : proj == 2 ? align_up(vsz_ * (size_t)n) : 0;
+    return ALIGN + proj_bytes + ws_bytes_for(path, n, G, K, dt);
 }
 
 // phase: 3 = whole call; 1 = zero + deposit only (multi-GPU split form);
@@ -485,11 +488,18 @@ int enqueue_multi(const int32_t *keys, const void *const *cols, int32_t ncols, i
         src[1] = cols[1];
         src[2] = dp;
         src[3] = charge;
+    } else if (proj == 2) {
+        void *sq = p;
+        p += align_up((dt == REPRO_F64 ? 8 : 4) * (size_t)n);
+        int rc = timed("project", st, [&] { return launch_square(dt, cols[0], n, sq, st, &t_launches); });
+        if (rc) return map_launch(rc);
+        src[0] = cols[0];
+        src[1] = sq;
     }
     const size_t rest = ws_bytes - (size_t)(p - (char *)ws);
     for (int c = 0; c < nout; ++c) {
         uint32_t *f = nullptr;
-        int rc = enqueue_groupby(keys, proj == 1 ? src[c] : cols[c], n, G, K, dt, outs[c], 0, nullptr, nullptr,
+        int rc = enqueue_groupby(keys, proj != 0 ? src[c] : cols[c], n, G, K, dt, outs[c], 0, nullptr, nullptr,
                                  nullptr, p, rest, st, &f);
         if (rc != REPRO_OK) return rc;
         rc = launch_flags_or(acc, f, st, &t_launches);
@@ -618,6 +628,33 @@ int repro_synth_generate(int32_t config, uint64_t seed, int64_t r0, int64_t n, i
         if (!cols[c]) return REPRO_EINVAL;
     const int rc = launch_synth(config, seed, r0, n, n_groups, keys, cols, (cudaStream_t)stream);
     return rc == -1 ? REPRO_EINVAL : map_launch(rc);
+}
+
+int repro_groupby_moments(const int32_t *keys, const void *vals, int64_t n, int32_t n_groups, int32_t fold,
+                          int32_t dtype, void *sum, void *avg, void *var, void *stddev, int64_t *counts) {
+    t_launches = 0;
+    if (!multi_valid(n, n_groups, 1, 2, fold, dtype) || !sum || !counts) return REPRO_EINVAL;
+    if (n > 0 && (!keys || !vals)) return REPRO_EINVAL;
+    const size_t vsz = dtype == REPRO_F64 ? 8 : 4;
+    const size_t need = multi_ws_bytes(n, n_groups, 1, 2, fold, dtype);
+    if (need == 0) return REPRO_EINVAL;
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    void *ws = cache_get(need + align_up(vsz * (size_t)n_groups));
+    if (!ws) return REPRO_ENOMEM;
+    void *sumsq = (char *)ws + need;  // SUM(x^2) lives after the multi workspace
+    void *outs[2] = {sum, sumsq};
+    const void *cols[1] = {vals};
+    uint32_t *flags = nullptr;
+    int rc = enqueue_multi(keys, cols, 1, 2, n, n_groups, fold, dtype, outs, counts, ws, need, 0, &flags);
+    if (rc == REPRO_OK)
+        rc = map_launch(timed("moments", 0, [&] {
+            return launch_moments(dtype, sum, sumsq, counts, n_groups, avg, var, stddev, 0, &t_launches);
+        }));
+    if (rc != REPRO_OK) {
+        cudaStreamSynchronize(0);
+        return rc;
+    }
+    return finish_blocking(flags, 0);
 }
 
 void repro_release_cache(void) {

@@ -48,6 +48,9 @@ int launch_q1_project(const double *price, const double *disc, const double *tax
                       double *charge, cudaStream_t st, int *launches);
 int launch_count_rows(const int32_t *keys, int64_t n, int32_t G, int64_t *counts, cudaStream_t st, int *launches);
 int launch_flags_or(uint32_t *acc, const uint32_t *f, cudaStream_t st, int *launches);
+int launch_square(int DT, const void *x, int64_t n, void *sq, cudaStream_t st, int *launches);
+int launch_moments(int DT, const void *s, const void *q, const int64_t *cnt, int32_t G, void *avg, void *var, void *sd,
+                   cudaStream_t st, int *launches);
 
 // device copy of synth.py's seeded generator (bench/test support, k_synth.cu)
 int launch_synth(int config, uint64_t seed, int64_t r0, int64_t n, int32_t G, int32_t *keys, void *const *cols,

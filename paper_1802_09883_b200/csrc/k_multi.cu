@@ -18,6 +18,7 @@ namespace repro {
 // back to one pass per column).
 int multi_virtual_columns(int proj, int ncols) {
     if (proj == 1) return ncols == 4 ? SrcQ1::NV : -1;
+    if (proj == 2) return ncols == 1 ? SrcMoments<1>::NV : -1;
     return (ncols == 1 || ncols == 2 || ncols == 4) ? ncols + 1 : -1;
 }
 
@@ -49,6 +50,12 @@ int launch_onchip_multi(int DT, int K, int proj, int ncols, const int32_t *keys,
     if (proj == 1) {
         if (DT != 1) return -1;
         MULTI_K(1, SrcQ1);
+    }
+    if (proj == 2) {
+        using M64 = SrcMoments<1>;
+        using M32 = SrcMoments<0>;
+        if (DT == 1) MULTI_K(1, M64);
+        MULTI_K(0, M32);
     }
     if (DT == 1) {
         if (ncols == 1) MULTI_K(1, C64_1);
@@ -110,6 +117,69 @@ __global__ void k_count_rows(const int32_t *__restrict__ keys, int64_t n, int32_
 }
 
 __global__ void k_flags_or(uint32_t *acc, const uint32_t *f) { *acc |= *f; }
+
+// x (x) x for the per-column fallback of the moments projection
+template <typename V>
+__global__ void k_square(const V *__restrict__ x, int64_t n, V *__restrict__ sq) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        sq[i] = sizeof(V) == 8 ? (V)__dmul_rn((double)x[i], (double)x[i]) : (V)__fmul_rn((float)x[i], (float)x[i]);
+}
+
+// AVG / sample VARIANCE / STDDEV from the reproducible SUM(x), SUM(x^2) and the
+// exact COUNT, each operation rounded once in a fixed order (so the outputs
+// are as reproducible as the sums):  avg = s / c,  var = max(0, (q - s*s/c) /
+// (c - 1)) (0 for c <= 1), stddev = sqrt(var); an empty group gives 0.
+template <typename V>
+__global__ void k_moments(const V *__restrict__ s, const V *__restrict__ q, const int64_t *__restrict__ cnt, int32_t G,
+                          V *avg, V *var, V *sd) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= G) return;
+    const int64_t c = cnt[g];
+    V a = V(0), v = V(0);
+    if (sizeof(V) == 8) {
+        const double cd = (double)c;
+        if (c > 0) a = (V)__ddiv_rn((double)s[g], cd);
+        if (c > 1) {
+            const double t = __dsub_rn((double)q[g], __ddiv_rn(__dmul_rn((double)s[g], (double)s[g]), cd));
+            v = (V)fmax(0.0, __ddiv_rn(t, __dsub_rn(cd, 1.0)));
+        }
+        if (avg) avg[g] = a;
+        if (var) var[g] = v;
+        if (sd) sd[g] = (V)__dsqrt_rn((double)v);
+    } else {
+        const float cf = __ll2float_rn(c);
+        if (c > 0) a = (V)__fdiv_rn((float)s[g], cf);
+        if (c > 1) {
+            const float t = __fsub_rn((float)q[g], __fdiv_rn(__fmul_rn((float)s[g], (float)s[g]), cf));
+            v = (V)fmaxf(0.0f, __fdiv_rn(t, __fsub_rn(cf, 1.0f)));
+        }
+        if (avg) avg[g] = a;
+        if (var) var[g] = v;
+        if (sd) sd[g] = (V)__fsqrt_rn((float)v);
+    }
+}
+
+int launch_square(int DT, const void *x, int64_t n, void *sq, cudaStream_t st, int *launches) {
+    if (n == 0) return 0;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * device_props().sms);
+    if (DT == 1) k_square<double><<<blocks, 256, 0, st>>>((const double *)x, n, (double *)sq);
+    else k_square<float><<<blocks, 256, 0, st>>>((const float *)x, n, (float *)sq);
+    ++*launches;
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+int launch_moments(int DT, const void *s, const void *q, const int64_t *cnt, int32_t G, void *avg, void *var, void *sd,
+                   cudaStream_t st, int *launches) {
+    const int blocks = (G + 255) / 256;
+    if (DT == 1)
+        k_moments<double><<<blocks, 256, 0, st>>>((const double *)s, (const double *)q, cnt, G, (double *)avg,
+                                                  (double *)var, (double *)sd);
+    else
+        k_moments<float><<<blocks, 256, 0, st>>>((const float *)s, (const float *)q, cnt, G, (float *)avg,
+                                                 (float *)var, (float *)sd);
+    ++*launches;
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
 
 int launch_multi_scatter(int DT, int K, const void *vout, int32_t G, int nsum, void *const *outs,
                          const unsigned long long *slots, int64_t *counts, cudaStream_t st, int *launches) {

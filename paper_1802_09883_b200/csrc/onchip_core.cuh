@@ -463,6 +463,27 @@ struct SrcQ1 {
     }
 };
 
+// Second moments (f2 of SURVEY.md 8(f): AVG / VARIANCE / STDDEV from SUMs,
+// PAPER.md:163-174): one column x -> SUM(x), SUM(x (x) x) (one rounding per
+// square), COUNT.
+template <int DT>
+struct SrcMoments {
+    using V = typename Fmt<DT>::V;
+    static constexpr int NCOL = 1, NV = 3;
+    static constexpr bool ONES = true;
+    static constexpr int R = ONCHIP_RMULTI;
+    const V *col[NCOL];
+    int G;
+    __device__ __forceinline__ void expand(int32_t key, const V (&c)[NCOL], int32_t (&vk)[NV], V (&vv)[NV]) const {
+        const bool ok = (uint32_t)key < (uint32_t)G;
+        vv[0] = c[0];
+        vv[1] = Fmt<DT>::mul(c[0], c[0]);
+        vv[2] = V(1);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) vk[j] = ok ? key + j * G : -1;
+    }
+};
+
 // Where a block's finished table goes: MODE 0 adds it into the absolute-level
 // slot table (kglob, slots); MODE 1 writes it densely as one partial state per
 // group (pk[g], pT[g*K + l]) for the partitioned path's merge.

@@ -154,3 +154,15 @@ def test_split_form_with_emulated_ranks(R):
     for x, y in zip(outs, ref):
         assert torch.equal(x, y)
     assert torch.equal(counts, rc)
+
+
+@pytest.mark.parametrize("dtype,G,n", [(np.float64, 10, 200003), (np.float32, 7, 100001), (np.float64, 700, 50001)])
+def test_moments_match_oracle(R, dtype, G, n):
+    rng = np.random.default_rng(G + n)
+    keys = rng.integers(0, G, n).astype(np.int32)
+    x = (rng.standard_normal(n) * 2.0 ** rng.integers(-10, 10, n)).astype(dtype)
+    res = R.groupby_moments(dev(keys), dev(x), G, 3 if dtype == np.float64 else 2)
+    rc, ref = O.groupby_moments(keys, x, G, 3 if dtype == np.float64 else 2)
+    assert rc == O.OK
+    for k in ("sum", "avg", "var", "stddev", "count"):
+        assert res[k].cpu().numpy().tobytes() == ref[k].tobytes(), k

@@ -78,3 +78,33 @@ def test_multi_error_precedence():
     assert rc == O.EKEY
     rc, _, _ = O.groupby_sum_multi(np.array([0, 1, 2], np.int32), [b, a], 3, 2)
     assert rc == O.EDOM
+
+
+def test_moments_exact_on_integer_data():
+    # small integers: the reproducible sums are exact, so AVG / VARIANCE follow
+    # from exact rationals rounded once per operation
+    rng = np.random.default_rng(12)
+    keys = rng.integers(0, 5, 3000).astype(np.int32)
+    x = rng.integers(-1000, 1000, 3000).astype(np.float64)
+    rc, m = O.groupby_moments(keys, x, 5, 3)
+    assert rc == O.OK
+    for g in range(5):
+        xs = [Fraction(int(v)) for v in x[keys == g]]
+        c = len(xs)
+        s, q = sum(xs), sum(v * v for v in xs)
+        assert m["sum"][g] == float(s) and m["count"][g] == c
+        assert m["avg"][g] == rn64(s / Fraction(c))
+        t = Fraction(float(q)) - Fraction(rn64(Fraction(float(s)) * Fraction(float(s)) / c))
+        want_var = max(0.0, rn64(Fraction(rn64(t)) / (c - 1)))
+        assert m["var"][g] == want_var
+        assert m["stddev"][g] == np.sqrt(want_var)
+
+
+def test_moments_special_counts():
+    keys = np.array([0, 1, 1], np.int32)
+    x = np.array([2.5, -1.0, 3.0])
+    rc, m = O.groupby_moments(keys, x, 3, 2)
+    assert rc == O.OK
+    assert m["count"].tolist() == [1, 2, 0]
+    assert m["avg"].tolist() == [2.5, 1.0, 0.0]
+    assert m["var"].tolist() == [0.0, 8.0, 0.0]  # ((9+1) - 4/2) / 1
