@@ -166,6 +166,22 @@ int repro_groupby_sum_multi(const int32_t *keys, const void *const *cols,
                             int32_t n_groups, int32_t fold, int32_t dtype,
                             void *const *outs, int64_t *counts);
 
+/* GroupBy-SUM over ARBITRARY int64 keys (the paper's
+ * operators hash keys): the keys are mapped to dense ids
+ * through a GPU hash table (open addressing, 2^b >= 2 max_groups slots), the
+ * distinct keys are sorted ascending, and the dense reproducible GroupBy runs
+ * on the ids.  Outputs: out_keys[0..d) = the distinct keys ascending,
+ * out_vals[0..d) = their reproducible sums (dtype), *n_groups_out = d.  Both
+ * depend only on the multiset of (key, value) pairs.  keys: DEVICE int64[n]
+ * (INT64_MIN is reserved: REPRO_EKEY); out_keys / out_vals: DEVICE arrays of
+ * max_groups elements.  More than max_groups distinct keys: REPRO_ENOMEM with
+ * *n_groups_out = the distinct count (retry with a larger capacity).  max_groups
+ * is limited by the dense path (2^26).  Blocking. */
+int repro_groupby_sum_sparse(const int64_t *keys, const void *vals, int64_t n,
+                             int64_t max_groups, int32_t fold, int32_t dtype,
+                             int64_t *out_keys, void *out_vals,
+                             int64_t *n_groups_out);
+
 /* AVG / sample VARIANCE / STDDEV per group from reproducible SUMs (SURVEY.md
  * 8(f) f2; the paper reduces every float aggregate to SUM):
  * one fused pass computes SUM(x), SUM(x*x) and COUNT (proj 2 above), then,

@@ -271,3 +271,22 @@ def groupby_moments(keys: np.ndarray, vals: np.ndarray, n_groups: int, fold: int
         var = np.where(c > 1, np.maximum(zero, np.divide(t, np.subtract(cf, one))), zero).astype(vals.dtype)
     sd = np.sqrt(var).astype(vals.dtype)
     return rc, {"sum": s, "avg": avg, "var": var, "stddev": sd, "count": c}
+
+
+INT64_MIN = np.iinfo(np.int64).min
+
+
+def groupby_sum_sparse(keys: np.ndarray, vals: np.ndarray, fold: int, *, threads: int | None = None):
+    """GroupBy-SUM over arbitrary int64 keys (the C-ABI's
+    repro_groupby_sum_sparse): the distinct keys ascending (np.unique) and O5
+    on the dense ids = rank of each row's key.  INT64_MIN is reserved (EKEY).
+    Returns (status, distinct keys, sums)."""
+    keys = np.ascontiguousarray(keys, dtype=np.int64)
+    if np.any(keys == INT64_MIN):
+        return EKEY, np.zeros(0, np.int64), np.zeros(0, vals.dtype)
+    uniq = np.unique(keys)
+    if uniq.size == 0:
+        return OK, uniq, np.zeros(0, vals.dtype)
+    ids = np.searchsorted(uniq, keys).astype(np.int32)
+    rc, out = groupby_sum(ids, vals, int(uniq.size), fold, threads=threads)
+    return rc, uniq, out

@@ -51,6 +51,7 @@ _sig("repro_synth_generate", ctypes.c_int, _i32, ctypes.c_uint64, _i64, _i64, _i
 _sig("repro_groupby_sum_multi", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
      ctypes.POINTER(_vp), _vp)
 _sig("repro_groupby_multi_workspace_bytes", _sz, _i64, _i32, _i32, _i32, _i32, _i32)
+_sig("repro_groupby_sum_sparse", ctypes.c_int, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp, ctypes.POINTER(_i64))
 _sig("repro_groupby_moments", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp)
 _sig("repro_groupby_multi_table", ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_i64),
      ctypes.POINTER(_i64))
@@ -227,6 +228,22 @@ def groupby_sum_multi(keys, cols, n_groups: int, fold: int = 3, proj: int = 0, o
                                       optr, cnt)
     _check(st, "repro_groupby_sum_multi")
     return outs, (counts if with_counts else None)
+
+
+def groupby_sum_sparse(keys, vals, max_groups: int, fold: int = 3):
+    """Reproducible GroupBy-SUM over arbitrary int64 keys (repro_groupby_sum_sparse).
+    Returns (distinct keys ascending, their sums) as device tensors."""
+    torch = _torch()
+    dt = _dtype_code(vals)
+    if keys.numel() != vals.numel():
+        raise ValueError("keys and vals differ in length")
+    ok = torch.empty(max_groups, dtype=torch.int64, device=vals.device)
+    ov = torch.empty(max_groups, dtype=vals.dtype, device=vals.device)
+    d = _i64()
+    _check(_lib.repro_groupby_sum_sparse(_dev(keys, "keys", torch.int64), _dev(vals, "vals"), keys.numel(), max_groups,
+                                         fold, dt, _dev(ok, "out_keys", torch.int64), _dev(ov, "out_vals", vals.dtype),
+                                         ctypes.byref(d)), "repro_groupby_sum_sparse")
+    return ok[: d.value], ov[: d.value]
 
 
 def groupby_moments(keys, vals, n_groups: int, fold: int = 3):

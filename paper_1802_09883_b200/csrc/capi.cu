@@ -630,6 +630,45 @@ int repro_synth_generate(int32_t config, uint64_t seed, int64_t r0, int64_t n, i
     return rc == -1 ? REPRO_EINVAL : map_launch(rc);
 }
 
+int repro_groupby_sum_sparse(const int64_t *keys, const void *vals, int64_t n, int64_t max_groups, int32_t fold,
+                             int32_t dtype, int64_t *out_keys, void *out_vals, int64_t *n_groups_out) {
+    t_launches = 0;
+    if (n < 0 || max_groups < 1 || max_groups > partition_max_groups(fold, dtype) || !valid_shape(1, fold, dtype) ||
+        !out_keys || !out_vals || !n_groups_out)
+        return REPRO_EINVAL;
+    if (n > 0 && (!keys || !vals)) return REPRO_EINVAL;
+    *n_groups_out = 0;
+    const int32_t gmax = (int32_t)max_groups;
+    const int pmax = choose_path(gmax, fold, dtype);
+    if (pmax < 0) return REPRO_EINVAL;
+    const int32_t gon = std::min<int32_t>(gmax, onchip_max_groups(fold, dtype));
+    const size_t dense = std::max(ws_bytes_for(pmax, n, gmax, fold, dtype), ws_bytes_for(0, n, gon, fold, dtype));
+    const size_t sp = align_up(sparse_scratch_bytes(n, max_groups));
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    void *ws = cache_get(ALIGN + sp + dense);
+    if (!ws) return REPRO_ENOMEM;
+    uint32_t *mflags = (uint32_t *)ws;
+    if (cudaMemsetAsync(mflags, 0, 4, 0) != cudaSuccess) return REPRO_ECUDA;
+    int32_t *ids = nullptr;
+    int64_t d = 0;
+    int rc = sparse_map_keys(keys, n, max_groups, (char *)ws + ALIGN, out_keys, &ids, &d, mflags, 0, &t_launches);
+    *n_groups_out = d;
+    if (rc == -1) return REPRO_ENOMEM;
+    if (rc) return REPRO_ECUDA;
+    uint32_t f = 0;
+    if (cudaMemcpy(&f, mflags, 4, cudaMemcpyDeviceToHost) != cudaSuccess) return REPRO_ECUDA;
+    if (f) return status_from_flags(f);
+    if (d == 0) return REPRO_OK;
+    uint32_t *flags = nullptr;
+    rc = enqueue_groupby(ids, vals, n, (int32_t)d, fold, dtype, out_vals, 0, nullptr, nullptr, nullptr,
+                         (char *)ws + ALIGN + sp, dense, 0, &flags);
+    if (rc != REPRO_OK) {
+        cudaStreamSynchronize(0);
+        return rc;
+    }
+    return finish_blocking(flags, 0);
+}
+
 int repro_groupby_moments(const int32_t *keys, const void *vals, int64_t n, int32_t n_groups, int32_t fold,
                           int32_t dtype, void *sum, void *avg, void *var, void *stddev, int64_t *counts) {
     t_launches = 0;

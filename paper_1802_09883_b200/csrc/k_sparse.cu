@@ -1,0 +1,171 @@
+// k_sparse.cu -- GroupBy-SUM over arbitrary int64 keys:
+// the paper's operators hash their keys (HashAggregation);
+// the dense path assumes identity hashing.  Here the keys are
+// first mapped to dense group ids through a GPU hash table, then the dense
+// reproducible GroupBy runs unchanged:
+//   1. k_hash_insert   open addressing (linear probing, 64-bit CAS) of every
+//                      row's key into a table of 2^b slots
+//   2. k_hash_collect  the distinct keys (in table order)
+//   3. sort            the distinct keys ascending (cub radix sort): the dense
+//                      id of a key is its rank, so ids -- and the output
+//                      order -- depend only on the SET of keys
+//   4. k_hash_assign   rank -> the key's slot
+//   5. k_hash_map      every row's id
+// The sums are the dense path's, so the result bits depend only on the
+// multiset of (key, value) pairs.  Slots hold key ^ 2^63 (0 = empty, so the
+// table is cleared with a memset); the key INT64_MIN is reserved (EKEY).
+#include <algorithm>
+
+#include <cub/device/device_radix_sort.cuh>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace repro {
+
+namespace {
+
+constexpr unsigned long long FLIP = 0x8000000000000000ull;
+
+__device__ __forceinline__ uint64_t fmix64(uint64_t k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+__global__ void k_hash_insert(const int64_t *__restrict__ keys, int64_t n, unsigned long long *tk, uint64_t mask,
+                              uint32_t *status, unsigned long long *distinct) {
+    uint32_t bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long s = (unsigned long long)keys[i] ^ FLIP;
+        if (s == 0ull) {
+            bad = FLAG_EKEY;
+            continue;
+        }
+        uint64_t h = fmix64(s) & mask;
+        // bounded probing: with more distinct keys than slots (the caller then
+        // reports ENOMEM from the distinct count) a row gives up after a full turn
+        for (uint64_t probe = 0; probe <= mask; ++probe) {
+            const unsigned long long cur = tk[h];
+            if (cur == s) break;
+            if (cur == 0ull) {
+                const unsigned long long prev = atomicCAS(&tk[h], 0ull, s);
+                if (prev == 0ull) {
+                    atomicAdd(distinct, 1ull);
+                    break;
+                }
+                if (prev == s) break;
+            }
+            h = (h + 1) & mask;
+        }
+    }
+    if (bad) atomicOr(status, bad);
+}
+
+__global__ void k_hash_collect(const unsigned long long *tk, uint64_t cap, int64_t *out, unsigned long long *count) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (uint64_t)gridDim.x * blockDim.x) {
+        const unsigned long long s = tk[i];
+        if (s != 0ull) out[atomicAdd(count, 1ull)] = (int64_t)(s ^ FLIP);
+    }
+}
+
+__device__ __forceinline__ uint64_t find_slot(const unsigned long long *tk, uint64_t mask, unsigned long long s) {
+    uint64_t h = fmix64(s) & mask;
+    while (tk[h] != s) h = (h + 1) & mask;  // every probed key is present
+    return h;
+}
+
+__global__ void k_hash_assign(const int64_t *__restrict__ sorted, int64_t d, const unsigned long long *tk,
+                              uint64_t mask, int32_t *tid) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x)
+        tid[find_slot(tk, mask, (unsigned long long)sorted[i] ^ FLIP)] = (int32_t)i;
+}
+
+__global__ void k_hash_map(const int64_t *__restrict__ keys, int64_t n, const unsigned long long *tk, uint64_t mask,
+                           const int32_t *__restrict__ tid, int32_t *ids) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long s = (unsigned long long)keys[i] ^ FLIP;
+        ids[i] = s == 0ull ? -1 : tid[find_slot(tk, mask, s)];
+    }
+}
+
+int grid_for(int64_t n) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 16 * (int64_t)device_props().sms));
+}
+
+size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+size_t sort_tmp_bytes(int64_t items) {
+    size_t tmp = 0;
+    cub::DeviceRadixSort::SortKeys(nullptr, tmp, (const int64_t *)nullptr, (int64_t *)nullptr,
+                                   (int)std::max<int64_t>(items, 1));
+    return tmp;
+}
+
+}  // namespace
+
+uint64_t sparse_table_slots(int64_t max_groups) {
+    uint64_t cap = 1024;
+    while (cap < 2 * (uint64_t)std::max<int64_t>(max_groups, 1)) cap <<= 1;
+    return cap;
+}
+
+size_t sparse_scratch_bytes(int64_t n, int64_t max_groups) {
+    const uint64_t cap = sparse_table_slots(max_groups);
+    const size_t mg = (size_t)std::max<int64_t>(max_groups, 1);
+    return al256(8 * cap) + al256(4 * cap) + al256(8 * mg) + al256(16) + al256(sort_tmp_bytes(max_groups)) +
+           al256(4 * (size_t)std::max<int64_t>(n, 1));
+}
+
+// Map the keys to dense ids (ascending key order); `sorted_out` receives the
+// distinct keys, *ids_out points at the int32 ids inside `scratch`, *d_out =
+// number of distinct keys (the call synchronises `st` to read it).  Returns
+// 0, -1 when there are more than max_groups distinct keys (*d_out still set),
+// -2 on a CUDA error.
+int sparse_map_keys(const int64_t *keys, int64_t n, int64_t max_groups, void *scratch, int64_t *sorted_out,
+                    int32_t **ids_out, int64_t *d_out, uint32_t *status, cudaStream_t st, int *launches) {
+    const uint64_t cap = sparse_table_slots(max_groups), mask = cap - 1;
+    const size_t mg = (size_t)std::max<int64_t>(max_groups, 1);
+    char *p = (char *)scratch;
+    unsigned long long *tk = (unsigned long long *)p;
+    p += al256(8 * cap);
+    int32_t *tid = (int32_t *)p;
+    p += al256(4 * cap);
+    int64_t *dk = (int64_t *)p;
+    p += al256(8 * mg);
+    unsigned long long *cnt = (unsigned long long *)p;  // [0] distinct (insert), [1] collected
+    p += al256(16);
+    const size_t tmp = sort_tmp_bytes(max_groups);
+    void *ctmp = p;
+    p += al256(tmp);
+    int32_t *ids = (int32_t *)p;
+    *ids_out = ids;
+    if (cudaMemsetAsync(tk, 0, 8 * cap, st) != cudaSuccess || cudaMemsetAsync(cnt, 0, 16, st) != cudaSuccess)
+        return -2;
+    if (n > 0) {
+        k_hash_insert<<<grid_for(n), 256, 0, st>>>(keys, n, tk, mask, status, cnt);
+        ++*launches;
+    }
+    unsigned long long d = 0;
+    if (cudaMemcpyAsync(&d, cnt, 8, cudaMemcpyDeviceToHost, st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess)
+        return -2;
+    *d_out = (int64_t)d;
+    if ((int64_t)d > max_groups) return -1;
+    if (d > 0) {
+        k_hash_collect<<<grid_for((int64_t)cap), 256, 0, st>>>(tk, cap, dk, cnt + 1);
+        ++*launches;
+        size_t t = tmp;
+        if (cub::DeviceRadixSort::SortKeys(ctmp, t, dk, sorted_out, (int)d, 0, 64, st) != cudaSuccess) return -2;
+        ++*launches;
+        k_hash_assign<<<grid_for((int64_t)d), 256, 0, st>>>(sorted_out, (int64_t)d, tk, mask, tid);
+        ++*launches;
+        k_hash_map<<<grid_for(n), 256, 0, st>>>(keys, n, tk, mask, tid, ids);
+        ++*launches;
+    }
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+}  // namespace repro

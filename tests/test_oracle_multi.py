@@ -108,3 +108,19 @@ def test_moments_special_counts():
     assert m["count"].tolist() == [1, 2, 0]
     assert m["avg"].tolist() == [2.5, 1.0, 0.0]
     assert m["var"].tolist() == [0.0, 8.0, 0.0]  # ((9+1) - 4/2) / 1
+
+
+def test_sparse_keys_dense_domain_equals_dense_groupby():
+    rng = np.random.default_rng(5)
+    keys = rng.integers(0, 50, 4000)
+    vals = rng.standard_normal(4000)
+    rc, uk, out = O.groupby_sum_sparse(keys, vals, 3)
+    assert rc == O.OK and np.array_equal(uk, np.unique(keys))
+    rc2, dense = O.groupby_sum(keys.astype(np.int32), vals, 50, 3)
+    assert out.tobytes() == dense[uk].tobytes()
+
+
+def test_sparse_keys_reserved_and_empty():
+    assert O.groupby_sum_sparse(np.array([3, O.INT64_MIN]), np.array([1.0, 2.0]), 2)[0] == O.EKEY
+    rc, uk, out = O.groupby_sum_sparse(np.zeros(0, np.int64), np.zeros(0), 2)
+    assert rc == O.OK and uk.size == 0 and out.size == 0
