@@ -1,4 +1,8 @@
 cd $GRAFT_REPO_ROOT
-python scripts/check_variants.py 2>&1 | cut -c1-200
-NOCHECK=1 GROUPS_LIST=16,256,1024 bash scripts/gpu_variants.sh; cat gpurun_out/variants.log | cut -c1-120
-for v in zs1 zs0; do export REPRO_B200_LIB=$PWD/scripts/variants/lib_$v.so; timeout 600 python bench.py --config 4 --steps 5 --warmup 3 --no-cpu-baseline --no-parity | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v c4', d['ms_per_step'])"; done
+O=gpurun_out/prof
+mkdir -p $O
+for c in 1 4; do
+  extra=""; [ $c = 4 ] && extra="--rows 268435456"
+  CMD="python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-parity $extra"
+  $CMD > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_c$c.csv $CMD > /dev/null 2>&1
+done
