@@ -31,6 +31,8 @@
 #include "onchip_core.cuh"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 namespace repro {
 
@@ -44,6 +46,9 @@ constexpr int SEG_NW = SEG_TPB / 32;
 constexpr int SEG_RT = 8;                    // rows per thread per scatter tile
 #ifndef SEG_RTH
 #define SEG_RTH 32                           // keys per thread in flight in the histogram
+#endif
+#ifndef PART_HEAVY
+#define PART_HEAVY 1                         // sum a partition with >= n/4 of the rows in place
 #endif
 #ifndef SEG_ONEPASS_BITS64
 #define SEG_ONEPASS_BITS64 8                 // binary64 rows: one pass up to 2^this partitions
@@ -59,6 +64,15 @@ constexpr size_t PALIGN = 256;
 
 inline size_t al(size_t x) { return (x + PALIGN - 1) / PALIGN * PALIGN; }
 
+// REPRO_DEBUG=1: synchronise and report the first CUDA error after each launch
+inline void dbg(const char *what) {
+    static const bool on = getenv("REPRO_DEBUG") != nullptr;
+    if (!on) return;
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "[repro] %s: %s\n", what, cudaGetErrorString(e));
+}
+
 struct Plan {
     int64_t ch;      // rows per work item (accumulate)
     int P;           // partitions holding groups: ceil(G / 1024)
@@ -71,6 +85,7 @@ struct Plan {
     int64_t max_units;
     int64_t max_items;
     int grid;        // persistent blocks of the hist / scatter kernels
+    int hb;          // work items of a heavy partition summed in place
 };
 
 Plan make_plan(int64_t n, int32_t G, int DT) {
@@ -98,7 +113,8 @@ Plan make_plan(int64_t n, int32_t G, int DT) {
     pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * sms, pl.max_units));
     // work items: ~8 per SM over the whole input, at least PART_CH rows
     pl.ch = std::max<int64_t>(PART_CH, (n + 8 * sms - 1) / (8 * sms));
-    pl.max_items = (n + pl.ch - 1) / pl.ch + pl.Pf;
+    pl.hb = 2 * sms;
+    pl.max_items = (n + pl.ch - 1) / pl.ch + pl.Pf + pl.hb;
     return pl;
 }
 
@@ -298,17 +314,37 @@ __global__ void __launch_bounds__(256) k_seg_scan(uint32_t *hist, const int32_t 
 }
 
 // single block: base[] = exclusive scan of ptot, pitem[] = exclusive scan of
-// the items per partition, then the item table
+// the items per partition, then the item table.  heavy_ok (last pass of a
+// one-pass plan, n >= 2^20): a partition holding >= n/4 of the rows (the
+// heaviest; ties: lowest id) is not scattered -- its rows keep no space in the
+// output (ctrl[2] = its id, the scatter skips them) and it gets HB items over
+// the ORIGINAL row range [0, n), which k_part_accumulate reads through a
+// partition filter (skewed keys: the hot partition is summed in place)
 __global__ void __launch_bounds__(1024) k_part_plan(const int64_t *ptot, int P, int64_t chunk_rows, int64_t *base,
-                                                    int64_t *pitem, int64_t *items, int32_t *iown, int32_t *ctrl) {
+                                                    int64_t *pitem, int64_t *items, int32_t *iown, int32_t *ctrl,
+                                                    int heavy_ok, int64_t n, int hb) {
     __shared__ int64_t wsum[2][32];
+    __shared__ unsigned long long s_best;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int per = (P + 1023) / 1024;
     const int p0 = min(tid * per, P), p1 = min(p0 + per, P);
+    if (tid == 0) s_best = 0ull;
+    __syncthreads();
+    if (heavy_ok) {
+        unsigned long long best = 0ull;  // (rows << 20) | (2^20 - 1 - p): max rows, then lowest p
+        for (int p = p0; p < p1; ++p)
+            best = max(best, ((unsigned long long)ptot[p] << 20) | (unsigned long long)((1 << 20) - 1 - p));
+        atomicMax(&s_best, best);
+    }
+    __syncthreads();
+    int heavy = -1;
+    if (heavy_ok && (int64_t)(s_best >> 20) * 4 >= n) heavy = (1 << 20) - 1 - (int)(s_best & ((1u << 20) - 1));
+    auto rows_of = [&](int p) { return p == heavy ? (int64_t)0 : ptot[p]; };
+    auto items_of = [&](int p) { return p == heavy ? (int64_t)hb : (ptot[p] + chunk_rows - 1) / chunk_rows; };
     int64_t rows = 0, its = 0;
     for (int p = p0; p < p1; ++p) {
-        rows += ptot[p];
-        its += (ptot[p] + chunk_rows - 1) / chunk_rows;
+        rows += rows_of(p);
+        its += items_of(p);
     }
     int64_t ir = rows, ii = its;
 #pragma unroll
@@ -323,13 +359,23 @@ __global__ void __launch_bounds__(1024) k_part_plan(const int64_t *ptot, int P, 
     for (int p = p0; p < p1; ++p) {
         base[p] = pr;
         pitem[p] = pi;
-        const int64_t c = (ptot[p] + chunk_rows - 1) / chunk_rows;
-        for (int64_t i = 0; i < c; ++i) {
-            items[2 * (pi + i)] = pr + i * chunk_rows;
-            items[2 * (pi + i) + 1] = min(pr + (i + 1) * chunk_rows, pr + ptot[p]);
-            iown[pi + i] = p;
+        const int64_t c = items_of(p);
+        if (p == heavy) {
+            // chunks of a multiple of 256 rows: every item starts 16-byte aligned (TMA ring)
+            const int64_t ch = ((n + hb - 1) / hb + 255) / 256 * 256;
+            for (int64_t i = 0; i < c; ++i) {
+                items[2 * (pi + i)] = min(n, i * ch);
+                items[2 * (pi + i) + 1] = min(n, (i + 1) * ch);
+                iown[pi + i] = p;
+            }
+        } else {
+            for (int64_t i = 0; i < c; ++i) {
+                items[2 * (pi + i)] = pr + i * chunk_rows;
+                items[2 * (pi + i) + 1] = min(pr + (i + 1) * chunk_rows, pr + ptot[p]);
+                iown[pi + i] = p;
+            }
         }
-        pr += ptot[p];
+        pr += rows_of(p);
         pi += c;
     }
     if (tid == 1023) {
@@ -337,6 +383,7 @@ __global__ void __launch_bounds__(1024) k_part_plan(const int64_t *ptot, int P, 
         pitem[P] = pi;
         ctrl[0] = (int32_t)pi;
         ctrl[1] = 0;
+        ctrl[2] = heavy;
     }
 }
 
@@ -351,8 +398,9 @@ __global__ void __launch_bounds__(SEG_TPB)
 k_seg_scatter(const int32_t *__restrict__ ikeys, const V *__restrict__ ivals, const int64_t *__restrict__ units,
               const int32_t *__restrict__ useg, const int32_t *__restrict__ ufirst, int S, int shift, int bits,
               int32_t G, int local, const uint32_t *__restrict__ hist, const int64_t *__restrict__ obase,
-              int32_t *__restrict__ okeys, V *__restrict__ ovals) {
+              int32_t *__restrict__ okeys, V *__restrict__ ovals, const int32_t *__restrict__ ctrl) {
     constexpr int TPB = SEG_TPB, NW = SEG_NW, RT = SEG_RT, TILE = SEG_TILE;
+    const int heavy = local ? ctrl[2] : -1;  // heavy partition: summed in place, not scattered
     extern __shared__ __align__(16) unsigned char sm[];
     V *sval = reinterpret_cast<V *>(sm);                          // [TILE]
     int32_t *skey = reinterpret_cast<int32_t *>(sval + TILE);     // [TILE]
@@ -387,8 +435,9 @@ k_seg_scatter(const int32_t *__restrict__ ikeys, const V *__restrict__ ivals, co
             }
 #pragma unroll
             for (int j = 0; j < RT; ++j) {
-                const bool valid = (uint32_t)kk[j] < (uint32_t)G;
+                bool valid = (uint32_t)kk[j] < (uint32_t)G;
                 dd[j] = valid ? (kk[j] >> shift) & (F - 1) : 0;
+                valid = valid && dd[j] != heavy;
                 const uint32_t m = peers_of(dd[j], bits, valid);
                 const uint32_t before = valid ? wh[warp * SEG_FMAX + dd[j]] : 0u;
                 rk[j] = valid ? before + __popc(m & ((1u << lane) - 1u)) : 0xFFFFFFFFu;
@@ -464,9 +513,10 @@ __global__ void __launch_bounds__(WS_TPB)
 k_seg_scatter_wide(const int32_t *__restrict__ ikeys, const V *__restrict__ ivals, const int64_t *__restrict__ units,
                    const int32_t *__restrict__ useg, const int32_t *__restrict__ ufirst, int S, int shift, int bits,
                    int32_t G, int local, const uint32_t *__restrict__ hist, const int64_t *__restrict__ obase,
-                   int32_t *__restrict__ okeys, V *__restrict__ ovals) {
+                   int32_t *__restrict__ okeys, V *__restrict__ ovals, const int32_t *__restrict__ ctrl) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int F = 1 << bits;
+    const int heavy = local ? ctrl[2] : -1;  // heavy partition: summed in place, not scattered
     uint32_t *cursor = reinterpret_cast<uint32_t *>(sm);  // [F] next output row (n < 2^32)
     uint32_t *tcnt = cursor + F;                           // [F] rows of the tile per digit
     uint32_t *tstart = tcnt + F;                           // [F] tile-local start
@@ -503,6 +553,7 @@ k_seg_scatter_wide(const int32_t *__restrict__ ikeys, const V *__restrict__ ival
 #pragma unroll
             for (int i = 0; i < WS_R; ++i) {
                 dd[i] = (uint32_t)kk[i] < (uint32_t)G ? (kk[i] >> shift) & (F - 1) : -1;
+                if (dd[i] == heavy) dd[i] = -1;
                 rk[i] = dd[i] >= 0 ? atomicAdd(&tcnt[dd[i]], 1u) : 0u;
             }
             __syncthreads();
@@ -571,9 +622,34 @@ k_part_accumulate(const int32_t *__restrict__ pkeys, const typename Fmt<DT>::V *
         const int p = iown[it];
         const int Gi = min(PART_GP, G - p * PART_GP);
         PubArgs out{nullptr, nullptr, pk + (size_t)it * PART_GP, pT + (size_t)it * PART_GP * K};
+        if (p == ctrl[2]) continue;  // heavy partition: k_part_heavy sums it in place
         const SrcSingle<DT> src{{pvals}, Gi};
         accumulate_range<DT, K, true, 1>(pkeys, src, items[2 * it], items[2 * it + 1], Gi, smem, flags, out);
     }
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if ((threadIdx.x & 31) == 0 && flags) atomicOr(status, flags);
+}
+
+// The heavy partition (k_part_plan): block b sums the rows of item
+// pitem[h] + b -- a range of the ORIGINAL columns -- through the partition
+// filter with the TMA-fed on-chip code, writing that item's partial states.
+// Launched unconditionally; blocks exit at once when there is no heavy
+// partition (the decision is on the device).
+template <int DT, int K, bool TMA>
+__global__ void __launch_bounds__(256, ONCHIP_MINBLOCKS)
+k_part_heavy(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals,
+             const int64_t *__restrict__ items, const int64_t *__restrict__ pitem, const int32_t *__restrict__ ctrl,
+             int32_t G, int32_t *pk, int64_t *pT, uint32_t *status) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int h = ctrl[2];
+    if (h < 0) return;
+    const int64_t it = pitem[h] + blockIdx.x;
+    if (it >= pitem[h + 1]) return;
+    const int Gi = min(PART_GP, G - h * PART_GP);
+    uint32_t flags = 0;
+    PubArgs out{nullptr, nullptr, pk + (size_t)it * PART_GP, pT + (size_t)it * PART_GP * K};
+    const SrcFiltered<DT> src{{vals}, Gi, h};
+    accumulate_range<DT, K, true, 1, TMA>(keys, src, items[2 * it], items[2 * it + 1], Gi, smem, flags, out);
     flags = __reduce_or_sync(0xffffffffu, flags);
     if ((threadIdx.x & 31) == 0 && flags) atomicOr(status, flags);
 }
@@ -678,8 +754,10 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
     if (n == 0) {
         cudaMemsetAsync(w.ptot, 0, 8 * (size_t)pl.Pf, st);
         int tp = trace_begin(st);
-        k_part_plan<<<1, 1024, 0, st>>>(w.ptot, pl.Pf, pl.ch, w.base, w.pitem, w.items, w.iown, w.ctrl);
+        k_part_plan<<<1, 1024, 0, st>>>(w.ptot, pl.Pf, pl.ch, w.base, w.pitem, w.items, w.iown, w.ctrl, 0, n,
+                                        pl.hb);
         trace_end(tp, "part_plan", st);
+            dbg("part_plan");
         ++*launches;
     } else {
         cudaFuncSetAttribute(k_seg_scatter<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
@@ -699,21 +777,25 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
             ++*launches;
             k_seg_scan<<<S * F, 256, 0, st>>>(w.hist, w.ufirst, bits, w.ptot);
             ++*launches;
-            k_part_plan<<<1, 1024, 0, st>>>(w.ptot, S * F, pl.ch, w.base, w.pitem, w.items, w.iown, w.ctrl);
+            const int heavy_ok = PART_HEAVY && pl.passes == 1 && n >= (1 << 20);
+            k_part_plan<<<1, 1024, 0, st>>>(w.ptot, S * F, pl.ch, w.base, w.pitem, w.items, w.iown, w.ctrl, heavy_ok,
+                                            n, pl.hb);
             ++*launches;
             trace_end(tk, "part_hist", st);
+            dbg("part_hist");
             tk = trace_begin(st);
             if (bits <= SEG_MAX_BITS) {
                 k_seg_scatter<V><<<pl.grid, SEG_TPB, ssm, st>>>(ik, iv, w.units, w.useg, w.ufirst, S, pl.shift[pass],
-                                                               bits, G, last ? 1 : 0, w.hist, w.base, ok, ov);
+                                                               bits, G, last ? 1 : 0, w.hist, w.base, ok, ov, w.ctrl);
             } else {
                 const size_t wsm = seg_scatter_wide_smem<V>(F);
                 cudaFuncSetAttribute(k_seg_scatter_wide<V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm);
                 k_seg_scatter_wide<V><<<pl.grid, WS_TPB, wsm, st>>>(ik, iv, w.units, w.useg, w.ufirst, S,
                                                                     pl.shift[pass], bits, G, last ? 1 : 0, w.hist,
-                                                                    w.base, ok, ov);
+                                                                    w.base, ok, ov, w.ctrl);
             }
             trace_end(tk, "part_scatter", st);
+            dbg("part_scatter");
             ++*launches;
             ik = ok;
             iv = ov;
@@ -731,7 +813,20 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
         kern<<<(unsigned)grid, 256, smem, st>>>(w.pkeys, (const V *)w.pvals, w.items, w.iown, w.ctrl, G, w.pk, w.pT,
                                                 status);
         trace_end(ta, "part_accumulate", st);
+            dbg("part_accumulate");
         ++*launches;
+        if (PART_HEAVY && pl.passes == 1 && n >= (1 << 20)) {
+            // the heavy partition (if the plan found one) straight from the input
+            const bool tma = ((((uintptr_t)keys) | ((uintptr_t)vals)) & 15) == 0;
+            auto hk = tma ? k_part_heavy<DT, K, true> : k_part_heavy<DT, K, false>;
+            const size_t hsm = onchip_smem_bytes<DT, K>(PART_GP, true, tma);
+            cudaFuncSetAttribute(hk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+            int th = trace_begin(st);
+            hk<<<pl.hb, 256, hsm, st>>>(keys, (const V *)vals, w.items, w.pitem, w.ctrl, G, w.pk, w.pT, status);
+            trace_end(th, "part_heavy", st);
+            dbg("part_heavy");
+            ++*launches;
+        }
     }
     int tk = trace_begin(st);
     const int64_t items_per_part = (pl.max_items + pl.P - 1) / pl.P;
@@ -739,6 +834,7 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
     k_part_merge<DT, K><<<(G + 31) / 32, 32 * mw, 0, st>>>(G, w.pitem, w.pk, w.pT, merge, acc_k, acc_C, acc_D,
                                                            (V *)out, status);
     trace_end(tk, "part_merge", st);
+            dbg("part_merge");
     ++*launches;
     return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }

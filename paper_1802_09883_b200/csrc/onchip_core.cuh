@@ -416,6 +416,26 @@ struct SrcSingle {
     }
 };
 
+// The rows of ONE partition (key >> 10 == part) read in place from the
+// original columns, as local keys 0..1023 of that partition; every other row
+// becomes (key 0, value 0), which deposits nothing and keeps the fast path
+// (the partitioned path's heavy-partition offload, k_partition.cu).
+template <int DT>
+struct SrcFiltered {
+    using V = typename Fmt<DT>::V;
+    static constexpr int NCOL = 1, NV = 1;
+    static constexpr bool ONES = false;
+    static constexpr int R = (DT == 1) ? ONCHIP_R64 : ONCHIP_R32;
+    const V *col[NCOL];
+    int G;     // groups of the partition (local keys)
+    int part;  // partition id
+    __device__ __forceinline__ void expand(int32_t key, const V (&c)[NCOL], int32_t (&vk)[NV], V (&vv)[NV]) const {
+        const bool in = key >= 0 && (key >> 10) == part;
+        vk[0] = in ? (key & 1023) : 0;
+        vv[0] = in ? c[0] : V(0);
+    }
+};
+
 // NC columns summed independently plus COUNT: virtual group j * G + g for
 // column j, and column NC holds the value 1 for every row (a reproducible sum
 // of ones is the exact row count).  Rows with a key outside [0, G) map to

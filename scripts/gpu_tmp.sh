@@ -1,8 +1,4 @@
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/prof
-mkdir -p $O
-for c in 1 4; do
-  extra=""; [ $c = 4 ] && extra="--rows 268435456"
-  CMD="python bench.py --config $c --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-parity $extra"
-  $CMD > /dev/null 2>&1 && ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches_c$c.csv $CMD > /dev/null 2>&1
-done
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "partition" 2>&1 | tail -3
+timeout 900 python bench.py --config 3 --steps 20 --warmup 3 --no-e2e --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c3', d['ms_per_step'], d['parity']['vs_oracle'], d.get('baseline_atomic',{}).get('slowdown_repro_vs_atomic'), {k:round(v,3) for k,v in d['per_kernel_ms'].items()})"
+for G in 16384 1048576; do timeout 600 python bench.py --config 2 --n-groups $G --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-atomic-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($G, d['ms_per_step'], {k:round(v,3) for k,v in d['per_kernel_ms'].items()})"; done

@@ -441,3 +441,25 @@ def test_partitioned_errors(R, partitioned):
     with pytest.raises(R.ReproError) as ei:
         gpu_groupby(R, keys, vals, 5000, 3)
     assert ei.value.status == R.EDOM
+
+
+@pytest.mark.parametrize("dtype,K,G,n", [(np.float64, 3, 1 << 16, (1 << 21) + 3), (np.float32, 2, 1 << 20, 1 << 22),
+                                         (np.float64, 2, 5000, 1 << 20)])
+def test_partitioned_heavy_partition_summed_in_place(R, dtype, K, G, n):
+    # Zipf keys: partition 0 holds far more than n/4 of the rows, so the plan
+    # sums it in place from the original columns instead of scattering it
+    keys, _ = synth.generate_chunked(3, n, G)
+    rng = np.random.default_rng(G)
+    vals = mixed_values(rng, n, dtype, 30)
+    bad = keys.copy()
+    R.set_path_override(1)
+    try:
+        got = gpu_groupby(R, keys, vals, G, K)
+        assert R.last_path() == 1
+        assert_bits_equal(got, oracle_groupby(keys, vals, G, K))
+        bad[n // 3] = G + 5  # an out-of-range key inside the heavy partition's key range is still EKEY
+        with pytest.raises(R.ReproError) as e:
+            gpu_groupby(R, bad, vals, G, K)
+        assert e.value.status == R.EKEY
+    finally:
+        R.set_path_override(-1)
