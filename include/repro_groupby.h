@@ -212,6 +212,32 @@ int repro_groupby_sum_multi_async(const int32_t *keys, const void *const *cols,
                                   int32_t *d_status);
 
 /* ------------------------------------------------------------------------
+ * Keyless single-array reproducible SUM and dot product (SURVEY.md 8(f) f4:
+ * the RSum algorithm's original setting, one group -- PAPER.md:755-757; the
+ * K-fold accumulator of Alg. 1, finalised by Eq. 1,
+ * PAPER.md:695-702).  x, y: DEVICE dtype[n], any alignment; the dot product
+ * deposits x[i] (x) y[i] (one rounding per product, reading A-19 of
+ * DESIGN.md).  out: DEVICE dtype[1].  The result is the same bits as
+ * repro_groupby_sum with every key 0 over x (or over the products), for any
+ * order, launch geometry or GPU count.  Status codes as repro_groupby_sum
+ * (NaN/Inf -> REPRO_EDOM; out then holds the IEEE sum of the specials).
+ * n == 0 writes +0.
+ * ---------------------------------------------------------------------- */
+int repro_sum(const void *x, int64_t n, int32_t fold, int32_t dtype, void *out);
+int repro_dot(const void *x, const void *y, int64_t n, int32_t fold,
+              int32_t dtype, void *out);
+
+/* Workspace bytes of repro_dot_async (0 on invalid fold / dtype). */
+size_t repro_dot_workspace_bytes(int32_t fold, int32_t dtype);
+
+/* Stream-ordered SUM (y == NULL) or dot product with the caller's workspace
+ * (>= repro_dot_workspace_bytes, 256-byte aligned) and device status word
+ * (conventions of repro_groupby_sum_async). */
+int repro_dot_async(const void *x, const void *y, int64_t n, int32_t fold,
+                    int32_t dtype, void *out, void *workspace,
+                    size_t ws_bytes, void *stream, int32_t *d_status);
+
+/* ------------------------------------------------------------------------
  * Accumulator handles: n_groups device-resident repro<ScalarT, fold> states
  * (the paper's intermediate aggregates).  A handle is not
  * thread-safe; distinct handles are independent.  All calls are blocking.

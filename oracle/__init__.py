@@ -273,6 +273,26 @@ def groupby_moments(keys: np.ndarray, vals: np.ndarray, n_groups: int, fold: int
     return rc, {"sum": s, "avg": avg, "var": var, "stddev": sd, "count": c}
 
 
+def rsum(x: np.ndarray, fold: int, *, threads: int | None = None):
+    """Reproducible SUM of one array -- the RSum setting:
+    one accumulator over every element (O5 with the single group 0).
+    Returns (status, value)."""
+    x = np.ascontiguousarray(x)
+    rc, out = groupby_sum(np.zeros(x.size, np.int32), x, 1, fold, threads=threads)
+    return rc, out[0]
+
+
+def dot(x: np.ndarray, y: np.ndarray, fold: int, *, threads: int | None = None):
+    """Reproducible dot product: each product x_i * y_i rounded once in the
+    value type (numpy elementwise multiply, reading A-19), then rsum.
+    Returns (status, value)."""
+    x, y = np.ascontiguousarray(x), np.ascontiguousarray(y)
+    assert x.dtype == y.dtype and x.size == y.size
+    with np.errstate(invalid="ignore", over="ignore"):
+        prod = np.multiply(x, y)
+    return rsum(prod, fold, threads=threads)
+
+
 INT64_MIN = np.iinfo(np.int64).min
 
 

@@ -61,6 +61,10 @@ _sig("repro_groupby_multi_finish_async", ctypes.c_int, _i64, _i32, _i32, _i32, _
      _vp, _sz, _vp, _vp)
 _sig("repro_groupby_sum_multi_async", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
      ctypes.POINTER(_vp), _vp, _vp, _sz, _vp, _vp)
+_sig("repro_sum", ctypes.c_int, _vp, _i64, _i32, _i32, _vp)
+_sig("repro_dot", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _vp)
+_sig("repro_dot_workspace_bytes", _sz, _i32, _i32)
+_sig("repro_dot_async", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _sz, _vp, _vp)
 _sig("repro_acc_create", ctypes.c_int, ctypes.POINTER(_vp), _i32, _i32, _i32)
 _sig("repro_acc_deposit", ctypes.c_int, _vp, _vp, _vp, _i64)
 _sig("repro_acc_merge", ctypes.c_int, _vp, _vp)
@@ -259,6 +263,48 @@ def groupby_moments(keys, vals, n_groups: int, fold: int = 3):
                                       dt, *[_dev(res[k], k, vals.dtype) for k in ("sum", "avg", "var", "stddev")],
                                       _dev(res["count"], "count", torch.int64)), "repro_groupby_moments")
     return res
+
+
+def sum(x, fold: int = 3, out=None):  # noqa: A001 -- the paper's operation name
+    """Reproducible SUM of one array (repro_sum, blocking): a 1-element
+    device tensor, the same bits as groupby_sum with every key 0."""
+    torch = _torch()
+    dt = _dtype_code(x)
+    if out is None:
+        out = torch.empty(1, dtype=x.dtype, device=x.device)
+    _check(_lib.repro_sum(_dev(x, "x"), x.numel(), fold, dt, _dev(out, "out", x.dtype)), "repro_sum")
+    return out
+
+
+def dot(x, y, fold: int = 3, out=None):
+    """Reproducible dot product sum_i x_i (x) y_i (repro_dot, blocking)."""
+    torch = _torch()
+    dt = _dtype_code(x)
+    if y.numel() != x.numel():
+        raise ValueError("x and y differ in length")
+    if out is None:
+        out = torch.empty(1, dtype=x.dtype, device=x.device)
+    _check(_lib.repro_dot(_dev(x, "x"), _dev(y, "y", x.dtype), x.numel(), fold, dt, _dev(out, "out", x.dtype)),
+           "repro_dot")
+    return out
+
+
+def dot_workspace_bytes(fold: int, dtype: int) -> int:
+    return _lib.repro_dot_workspace_bytes(fold, dtype)
+
+
+def dot_async(x, y, fold: int, out, workspace, status, stream=None):
+    """Stream-ordered SUM (y None) or dot product (repro_dot_async)."""
+    torch = _torch()
+    dt = _dtype_code(x)
+    if y is not None and y.numel() != x.numel():
+        raise ValueError("x and y differ in length")
+    wp, wb = _aligned_ptr(workspace)
+    st = _lib.repro_dot_async(_dev(x, "x"), None if y is None else _dev(y, "y", x.dtype), x.numel(), fold, dt,
+                              _dev(out, "out", x.dtype), wp, wb, _stream_ptr(stream),
+                              _dev(status, "status", torch.int32))
+    _check(st, "repro_dot_async")
+    return out
 
 
 def multi_workspace_bytes(n: int, n_groups: int, ncols: int, proj: int, fold: int, dtype: int) -> int:

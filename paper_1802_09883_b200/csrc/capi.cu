@@ -696,6 +696,85 @@ int repro_groupby_moments(const int32_t *keys, const void *vals, int64_t n, int3
     return finish_blocking(flags, 0);
 }
 
+// ---- keyless single-array SUM / dot product (f4) ----------------------------
+
+size_t repro_dot_workspace_bytes(int32_t fold, int32_t dtype) {
+    return valid_shape(1, fold, dtype) ? onchip_ws_bytes(0, 1, fold, dtype) : 0;
+}
+
+}  // extern "C"
+
+namespace {
+
+int enqueue_array(const void *x, const void *y, int64_t n, int32_t K, int32_t dt, void *out, void *ws,
+                  cudaStream_t st, uint32_t **flags_out) {
+    OnchipWs w = carve_onchip(ws, n, 1, K, dt);
+    *flags_out = w.flags;
+    t_path = 0;
+    if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
+    // register-state kernel (k_array.cu) for 16-byte aligned arrays; the
+    // keyless on-chip kernel otherwise (or when a kernel variant is forced)
+    const bool aligned = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
+    int rc = (aligned && onchip_variant() == 0)
+                 ? timed("rsum", st, [&] {
+                       return launch_rsum(dt, K, x, y, n, w.kglob, w.slots, w.flags, st, &t_launches);
+                   })
+                 : timed("onchip_accumulate", st, [&] {
+                       return launch_onchip_array(dt, K, x, y, n, w.kglob, w.slots, w.flags, st, &t_launches);
+                   });
+    if (rc) return map_launch(rc);
+    return map_launch(timed("fold", st, [&] {
+        return launch_fold(dt, K, 1, w.kglob, w.slots, 0, nullptr, nullptr, nullptr, out, w.flags, st,
+                           &t_launches);
+    }));
+}
+
+int array_blocking(const void *x, const void *y, int64_t n, int32_t fold, int32_t dtype, void *out) {
+    t_launches = 0;
+    if (n < 0 || !valid_shape(1, fold, dtype) || !out || (n > 0 && !x)) return REPRO_EINVAL;
+    const size_t need = repro_dot_workspace_bytes(fold, dtype);
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    void *ws = cache_get(need);
+    if (!ws) return REPRO_ENOMEM;
+    uint32_t *flags = nullptr;
+    int rc = enqueue_array(x, y, n, fold, dtype, out, ws, 0, &flags);
+    if (rc != REPRO_OK) {
+        cudaStreamSynchronize(0);
+        return rc;
+    }
+    return finish_blocking(flags, 0);
+}
+
+}  // namespace
+
+extern "C" {
+
+int repro_dot_async(const void *x, const void *y, int64_t n, int32_t fold, int32_t dtype, void *out,
+                    void *workspace, size_t ws_bytes, void *stream, int32_t *d_status) {
+    t_launches = 0;
+    if (n < 0 || !valid_shape(1, fold, dtype) || !out || !workspace || !d_status || (n > 0 && !x))
+        return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    if (ws_bytes < repro_dot_workspace_bytes(fold, dtype)) return REPRO_ENOMEM;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *flags = nullptr;
+    int rc = enqueue_array(x, y, n, fold, dtype, out, workspace, st, &flags);
+    if (rc != REPRO_OK) return rc;
+    return map_launch(timed("status", st, [&] { return launch_status(flags, d_status, st, &t_launches); }));
+}
+
+int repro_sum(const void *x, int64_t n, int32_t fold, int32_t dtype, void *out) {
+    return array_blocking(x, nullptr, n, fold, dtype, out);
+}
+
+int repro_dot(const void *x, const void *y, int64_t n, int32_t fold, int32_t dtype, void *out) {
+    if (n > 0 && !y) {
+        t_launches = 0;
+        return REPRO_EINVAL;
+    }
+    return array_blocking(x, y, n, fold, dtype, out);
+}
+
 void repro_release_cache(void) {
     {
         std::lock_guard<std::mutex> lock(g_host.mu);

@@ -22,6 +22,7 @@ inline int slot_count(int DT, int K) { return (DT == 1 ? 25 : 7) + K; }
 // ---- launchers (return 0 on success, -1 unsupported shape, -2 CUDA error) --
 int onchip_max_groups(int K, int DT);
 void set_onchip_variant(int v);
+int onchip_variant();  // 0 auto, 1 atomic, 2 sorted, 3 atomic + register loads
 int sorted_max_groups(int K, int DT);
 int atomic_max_groups(int K, int DT);
 int launch_sorted_any(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
@@ -38,6 +39,10 @@ int launch_onchip_any(int DT, int K, const int32_t *keys, const void *vals, int6
 // (proj, ncols) shape (-1: no fused kernel), and the launcher over G real
 // groups (virtual groups j * G + g; -1 if this shape cannot run fused)
 int multi_virtual_columns(int proj, int ncols);
+int launch_rsum(int DT, int K, const void *x, const void *y, int64_t n, int32_t *kglob, unsigned long long *slots,
+                uint32_t *status, cudaStream_t st, int *launches);
+int launch_onchip_array(int DT, int K, const void *x, const void *y, int64_t n, int32_t *kglob,
+                        unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches);
 int launch_onchip_multi(int DT, int K, int proj, int ncols, const int32_t *keys, const void *const *cols, int64_t n,
                         int32_t G, int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
                         int *launches);

@@ -70,6 +70,33 @@ int launch_onchip_multi(int DT, int K, int proj, int ncols, const int32_t *keys,
     return -1;
 }
 
+// Keyless single-array SUM (y == nullptr) or dot product x . y (f4): one
+// group, no key column (SrcArray), counters with one copy per lane.
+int launch_onchip_array(int DT, int K, const void *x, const void *y, int64_t n, int32_t *kglob,
+                        unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches) {
+#define ARRAY_K(dt, NC)                                                                                          \
+    do {                                                                                                         \
+        SrcArray<dt, NC> src;                                                                                    \
+        src.col[0] = (const typename Fmt<dt>::V *)x;                                                             \
+        if (NC == 2) src.col[NC - 1] = (const typename Fmt<dt>::V *)y;                                           \
+        src.G = 1;                                                                                               \
+        switch (K) {                                                                                             \
+            case 1: return launch_onchip_src<dt, 1, SrcArray<dt, NC>, false>(nullptr, src, n, 1, kglob, slots, status, st, launches); \
+            case 2: return launch_onchip_src<dt, 2, SrcArray<dt, NC>, false>(nullptr, src, n, 1, kglob, slots, status, st, launches); \
+            case 3: return launch_onchip_src<dt, 3, SrcArray<dt, NC>, false>(nullptr, src, n, 1, kglob, slots, status, st, launches); \
+            case 4: return launch_onchip_src<dt, 4, SrcArray<dt, NC>, false>(nullptr, src, n, 1, kglob, slots, status, st, launches); \
+        }                                                                                                        \
+        return -1;                                                                                               \
+    } while (0)
+    if (DT == 1) {
+        if (y) ARRAY_K(1, 2);
+        ARRAY_K(1, 1);
+    }
+    if (y) ARRAY_K(0, 2);
+    ARRAY_K(0, 1);
+#undef ARRAY_K
+}
+
 // ---- helpers of the multi-column entry points ------------------------------
 
 struct OutPtrs {

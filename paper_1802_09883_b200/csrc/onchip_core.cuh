@@ -407,12 +407,31 @@ struct SrcSingle {
     using V = typename Fmt<DT>::V;
     static constexpr int NCOL = 1, NV = 1;
     static constexpr bool ONES = false;  // last virtual column constant 1 (COUNT)
+    static constexpr bool KEYLESS = false;  // no key column: every row is group 0
     static constexpr int R = (DT == 1) ? ONCHIP_R64 : ONCHIP_R32;
     const V *col[NCOL];
     int G;
     __device__ __forceinline__ void expand(int32_t key, const V (&c)[NCOL], int32_t (&vk)[NV], V (&vv)[NV]) const {
         vk[0] = key;
         vv[0] = c[0];
+    }
+};
+
+// Single-array reproducible SUM / dot product (f4 of SURVEY.md 8(f): the
+// original setting of the RSum algorithm): no key column,
+// every row is group 0; NCOL = 2 multiplies the two columns (one rounding).
+template <int DT, int NC>
+struct SrcArray {
+    using V = typename Fmt<DT>::V;
+    static constexpr int NCOL = NC, NV = 1;
+    static constexpr bool ONES = false;
+    static constexpr bool KEYLESS = true;
+    static constexpr int R = (DT == 1) ? ONCHIP_R64 : ONCHIP_R32;
+    const V *col[NCOL];
+    int G;
+    __device__ __forceinline__ void expand(int32_t, const V (&c)[NCOL], int32_t (&vk)[NV], V (&vv)[NV]) const {
+        vk[0] = 0;
+        vv[0] = NC == 2 ? Fmt<DT>::mul(c[0], c[NC - 1]) : c[0];
     }
 };
 
@@ -425,6 +444,7 @@ struct SrcFiltered {
     using V = typename Fmt<DT>::V;
     static constexpr int NCOL = 1, NV = 1;
     static constexpr bool ONES = false;
+    static constexpr bool KEYLESS = false;
     static constexpr int R = (DT == 1) ? ONCHIP_R64 : ONCHIP_R32;
     const V *col[NCOL];
     int G;     // groups of the partition (local keys)
@@ -445,6 +465,7 @@ struct SrcCols {
     using V = typename Fmt<DT>::V;
     static constexpr int NCOL = NC, NV = NC + 1;
     static constexpr bool ONES = true;
+    static constexpr bool KEYLESS = false;
     static constexpr int R = ONCHIP_RMULTI;
     const V *col[NCOL];
     int G;
@@ -466,6 +487,7 @@ struct SrcQ1 {
     using V = double;
     static constexpr int NCOL = 4, NV = 5;
     static constexpr bool ONES = true;
+    static constexpr bool KEYLESS = false;
     static constexpr int R = ONCHIP_RMULTI;
     const double *col[NCOL];
     int G;
@@ -491,6 +513,7 @@ struct SrcMoments {
     using V = typename Fmt<DT>::V;
     static constexpr int NCOL = 1, NV = 3;
     static constexpr bool ONES = true;
+    static constexpr bool KEYLESS = false;
     static constexpr int R = ONCHIP_RMULTI;
     const V *col[NCOL];
     int G;
@@ -534,7 +557,8 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
     // per INPUT row (virtual group j * G + g only gets column j of rows with
     // key g), so the limb headroom is counted in input rows
     constexpr int VTILE = TILE;
-    constexpr size_t ROWB = 4 + NCOL * sizeof(V);  // bytes per input row in a ring stage
+    constexpr size_t KB = SRC::KEYLESS ? 0 : 4;      // key bytes per input row
+    constexpr size_t ROWB = KB + NCOL * sizeof(V);  // bytes per input row in a ring stage
     static_assert(TILE <= Cfg::LIMIT, "tile larger than limb headroom");
     const int gq = onchip_gq<DT, K>(G, REGTOT);
     const int nq = gq >> 2;  // group quads
@@ -650,7 +674,7 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
             V c[NCOL];
 #pragma unroll
             for (int j = 0; j < NCOL; ++j) c[j] = in ? __ldg(src.col[j] + r) : V(0);
-            expand_row(i, in, in ? __ldg(keys + r) : -1, c, key, val);
+            expand_row(i, in, in ? (SRC::KEYLESS ? 0 : __ldg(keys + r)) : -1, c, key, val);
         }
     };
     // TMA-fed variant: full tiles stream through a ring of STAGES shared
@@ -667,10 +691,10 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
     auto issue = [&](int64_t t_base, int st) {  // thread 0 only; full tiles only
         const uint32_t bar = ring + 8u * st;
         mbar_expect_tx(bar, (uint32_t)(TILE * ROWB));
-        tma_load_1d(stage_keys(st), keys + t_base, TILE * 4, bar);
+        if (!SRC::KEYLESS) tma_load_1d(stage_keys(st), keys + t_base, TILE * 4, bar);
 #pragma unroll
         for (int j = 0; j < NCOL; ++j)
-            tma_load_1d(stage_keys(st) + (uint32_t)(TILE * (4 + j * sizeof(V))), src.col[j] + t_base,
+            tma_load_1d(stage_keys(st) + (uint32_t)(TILE * (KB + j * sizeof(V))), src.col[j] + t_base,
                         TILE * sizeof(V), bar);
     };
     if (TMA) {
@@ -694,13 +718,13 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
             const int st = tile % S;
             mbar_wait(ring + 8u * st, (uint32_t)((tile / S) & 1));
             const int32_t *sk = reinterpret_cast<const int32_t *>(smem + tbytes + 128 + (size_t)st * TILE * ROWB);
-            const V *sv = reinterpret_cast<const V *>(sk + TILE);
+            const V *sv = reinterpret_cast<const V *>(reinterpret_cast<const unsigned char *>(sk) + TILE * KB);
 #pragma unroll
             for (int i = 0; i < RIN; ++i) {
                 V c[NCOL];
 #pragma unroll
                 for (int j = 0; j < NCOL; ++j) c[j] = sv[j * TILE + tid + i * TPB];
-                expand_row(i, true, sk[tid + i * TPB], c, key, val);
+                expand_row(i, true, SRC::KEYLESS ? 0 : sk[tid + i * TPB], c, key, val);
             }
         } else {
             load_tile(base, key, val);

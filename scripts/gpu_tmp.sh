@@ -1,4 +1,3 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "partition" 2>&1 | tail -3
-timeout 900 python bench.py --config 3 --steps 20 --warmup 3 --no-e2e --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c3', d['ms_per_step'], d['parity']['vs_oracle'], d.get('baseline_atomic',{}).get('slowdown_repro_vs_atomic'), {k:round(v,3) for k,v in d['per_kernel_ms'].items()})"
-for G in 16384 1048576; do timeout 600 python bench.py --config 2 --n-groups $G --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-atomic-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($G, d['ms_per_step'], {k:round(v,3) for k,v in d['per_kernel_ms'].items()})"; done
+timeout 900 python -m pytest tests/test_gpu_array.py -q -x 2>&1 | tail -3
+timeout 300 python scripts/array_perf.py
