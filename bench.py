@@ -48,7 +48,11 @@ WORKLOADS = {
     3: "config3: 2^28 rows, keys Zipf(1.1) over 2^20, fp32 normal*2^e e in [-10,10], K=2",
     4: "config4: 2^30 rows, keys U[0,4), fp64 qty/price/disc/tax, 4 repro SUMs (qty, price, price*(1-disc), "
        "price*(1-disc)*(1+tax)) + COUNT, K=3 (fused multi-column pass)",
+    5: "f4 sum: 2^28 fp64 values +-(1+mant)2^e e in [-20,20] (config-1 values), keyless reproducible SUM, K=3",
+    6: "f4 dot: 2^27 x 2 fp64 vectors +-(1+mant)2^e e in [-20,20], reproducible dot product, K=3",
 }
+# f4: keyless single-array SUM / dot -- extra workloads, not BASELINE configs
+ARRAY = {5: dict(n=1 << 28, dot=False), 6: dict(n=1 << 27, dot=True)}
 ORACLE_SAMPLE_ROWS = 1 << 27  # bounded oracle sample (cpu_baseline): <= 2^27 rows, well under 30 s of host work
 PARITY_ROWS_MULTI = 1 << 24   # config 4: rows of the full input re-run on both sides for the parity check
 
@@ -71,6 +75,8 @@ def parse():
 
 def shape(args):
     from paper_1802_09883_b200 import synth
+    if args.config in ARRAY:
+        return args.rows or ARRAY[args.config]["n"], 1, 3, "f64"
     c = synth.CONFIGS[args.config]
     n = args.rows or c["n"]
     G = args.n_groups or c["n_groups"] or 1024
@@ -80,6 +86,11 @@ def shape(args):
 def host_rows(config, r0, n, G):
     """Host copy of rows [r0, r0+n) of a config (numpy generator)."""
     from paper_1802_09883_b200 import synth
+    if config in ARRAY:  # values of config 1 (x) and of a second seed (y); no keys
+        cols = [synth.generate(1, n=n, r0=r0)[1]]
+        if ARRAY[config]["dot"]:
+            cols.append(synth.generate(1, n=n, r0=r0, seed=synth.SEED_BASE + config)[1])
+        return None, cols
     if config == 3:
         seed = synth.SEED_BASE + 3
         keys = np.empty(n, np.int32)
@@ -106,6 +117,12 @@ def host_rows(config, r0, n, G):
 def device_rows(R, torch, config, r0, n, G):
     """Device-resident rows: generated on the GPU where the device generator
     exists (configs 0/1/2/4, bit-identical to synth.py), else uploaded."""
+    if config in ARRAY:
+        from paper_1802_09883_b200 import synth
+        cols = [R.synth_generate(1, n, 1024, r0=r0)[1][0]]
+        if ARRAY[config]["dot"]:
+            cols.append(R.synth_generate(1, n, 1024, r0=r0, seed=synth.SEED_BASE + config)[1][0])
+        return None, cols
     if config in (0, 1, 2, 4):
         return R.synth_generate(config, n, G, r0=r0)
     keys, cols = host_rows(config, r0, n, G)
@@ -185,6 +202,9 @@ class ClockSampler:
 def oracle_run(config, keys, cols, G, K, threads):
     """The oracle on host rows: (status, [outputs], counts or None)."""
     import oracle as O
+    if config in ARRAY:
+        rc, v = O.dot(cols[0], cols[1], K, threads=threads) if len(cols) == 2 else O.rsum(cols[0], K, threads=threads)
+        return rc, [np.array([v])], None
     if config == 4:
         return O.groupby_sum_multi(keys, cols, G, K, proj=1, threads=threads)
     rc, out = O.groupby_sum(keys, cols[0], G, K, threads=threads)
@@ -223,6 +243,8 @@ def reference_arm(args):
     sample = max(1 << 12, min(n, budget // steps))
     threads = O.default_threads()
     keys, cols = host_rows(args.config, 0, min(n, sample * steps), G)
+    if keys is None:
+        keys = np.zeros(cols[0].size, np.int32)  # placeholder for slicing (keyless workloads)
     for _ in range(args.warmup):
         oracle_run(args.config, keys[: 1 << 12], [c[: 1 << 12] for c in cols], G, K, threads)
     times = []
@@ -269,13 +291,18 @@ def main():
     dt = R.F64 if dts == "f64" else R.F32
     vsz = 8 if dt == R.F64 else 4
     multi = args.config == 4
-    ncol = 4 if multi else 1
-    row_bytes = 4 + ncol * vsz
+    array = args.config in ARRAY
+    ncol = 4 if multi else (2 if array and ARRAY[args.config]["dot"] else 1)
+    row_bytes = (0 if array else 4) + ncol * vsz
     keys, cols = device_rows(R, torch, args.config, rank * n, n, G)
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     status = torch.zeros(1, dtype=torch.int32, device="cuda")
-    if multi:
+    if array:
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+        ws = R.make_dot_workspace(K, dt)
+        ycol = cols[1] if ncol == 2 else None
+    elif multi:
         outs = [torch.empty(G, dtype=torch.float64, device="cuda") for _ in range(4)]
         counts = torch.empty(G, dtype=torch.int64, device="cuda")
         ws = R.make_multi_workspace(n, G, 4, 1, K, dt)
@@ -284,9 +311,15 @@ def main():
         ws = R.make_workspace(n, G, K, dt)
 
     from paper_1802_09883_b200 import dist as rdist
-    acc = R.Accumulator(G, K, dt) if (world > 1 and not multi) else None
+    acc = R.Accumulator(G, K, dt) if (world > 1 and not multi and not array) else None
 
     def step():
+        if array:
+            if world == 1:
+                R.dot_async(cols[0], ycol, K, out, ws, status, stream)
+            else:  # deposit, all-reduce the integer slot table, read out on every rank
+                rdist.dot_dist(R, cols[0], ycol, K, out, ws, status, stream=stream)
+            return
         if multi:
             if world == 1:
                 R.groupby_sum_multi_async(keys, cols, G, K, 1, outs, counts, ws, status, stream)
@@ -365,7 +398,7 @@ def main():
     }
 
     # ---- non-reproducible atomicAdd baseline on the same GPU -------------------
-    if not args.no_atomic_baseline and world == 1 and not multi:
+    if not args.no_atomic_baseline and world == 1 and not multi and not array:
         best = None
         for variant in (0, 1):
             try:
@@ -390,7 +423,7 @@ def main():
                                        "slowdown_repro_vs_atomic": ms_per_step / best[1]}
 
     # ---- end-to-end through the C-ABI with host buffers ---------------------
-    if not args.no_e2e and world == 1 and not multi:
+    if not args.no_e2e and world == 1 and not multi and not array:
         kp = keys.cpu().pin_memory()
         vp = cols[0].cpu().pin_memory()
         R.groupby_sum_host(kp, vp, G, K)
@@ -420,7 +453,13 @@ def main():
         line["cpu_baseline"] = cpu_baseline(args, n, G, K)
     if rank == 0 and world == 1 and not args.no_parity:
         import oracle as O
-        if multi:
+        if array:
+            _, hc = host_rows(args.config, 0, n, G)
+            rc, ref, _ = oracle_run(args.config, None, hc, G, K, O.default_threads())
+            got = out.cpu().numpy()
+            line["parity"] = {"vs_oracle": "bit-exact" if (rc == 0 and got.tobytes() == ref[0].tobytes())
+                              else "MISMATCH", "rows_compared": n}
+        elif multi:
             # full-size run is compared on its leading rows: GPU and oracle both
             # recompute rows [0, P) exactly
             P = min(n, PARITY_ROWS_MULTI)

@@ -237,6 +237,22 @@ int repro_dot_async(const void *x, const void *y, int64_t n, int32_t fold,
                     int32_t dtype, void *out, void *workspace,
                     size_t ws_bytes, void *stream, int32_t *d_status);
 
+/* Multi-GPU split form of repro_dot_async (conventions of the
+ * repro_groupby_multi_* split form): repro_dot_table gives the byte offsets
+ * (from the 256-aligned workspace start) and element counts of the status
+ * word (int32[1]), the window top (int32[1]) and the absolute-level slot
+ * table (int64[2 * (KMAX + fold)]); after repro_dot_deposit_async on every
+ * rank, all-reduce them (status bits OR, top MAX, slots SUM -- integer
+ * operations, any order) and call repro_dot_finish_async. */
+int repro_dot_table(int32_t fold, int32_t dtype, int64_t *offsets,
+                    int64_t *counts);
+int repro_dot_deposit_async(const void *x, const void *y, int64_t n,
+                            int32_t fold, int32_t dtype, void *workspace,
+                            size_t ws_bytes, void *stream);
+int repro_dot_finish_async(int32_t fold, int32_t dtype, void *out,
+                           void *workspace, size_t ws_bytes, void *stream,
+                           int32_t *d_status);
+
 /* ------------------------------------------------------------------------
  * Accumulator handles: n_groups device-resident repro<ScalarT, fold> states
  * (the paper's intermediate aggregates).  A handle is not

@@ -65,6 +65,9 @@ _sig("repro_sum", ctypes.c_int, _vp, _i64, _i32, _i32, _vp)
 _sig("repro_dot", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _vp)
 _sig("repro_dot_workspace_bytes", _sz, _i32, _i32)
 _sig("repro_dot_async", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _sz, _vp, _vp)
+_sig("repro_dot_table", ctypes.c_int, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64))
+_sig("repro_dot_deposit_async", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _vp, _sz, _vp)
+_sig("repro_dot_finish_async", ctypes.c_int, _i32, _i32, _vp, _vp, _sz, _vp, _vp)
 _sig("repro_acc_create", ctypes.c_int, ctypes.POINTER(_vp), _i32, _i32, _i32)
 _sig("repro_acc_deposit", ctypes.c_int, _vp, _vp, _vp, _i64)
 _sig("repro_acc_merge", ctypes.c_int, _vp, _vp)
@@ -304,6 +307,42 @@ def dot_async(x, y, fold: int, out, workspace, status, stream=None):
                               _dev(out, "out", x.dtype), wp, wb, _stream_ptr(stream),
                               _dev(status, "status", torch.int32))
     _check(st, "repro_dot_async")
+    return out
+
+
+def make_dot_workspace(fold: int, dtype: int, device="cuda"):
+    torch = _torch()
+    nbytes = dot_workspace_bytes(fold, dtype)
+    if nbytes == 0:
+        raise ReproError(EINVAL, "repro_dot_workspace_bytes")
+    return torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+
+
+def dot_table_views(workspace, fold: int, dtype: int):
+    """(flags int32[1], kglob int32[1], slots int64[...]) views of the slot
+    table inside a dot workspace (make_dot_workspace)."""
+    torch = _torch()
+    off, cnt = (_i64 * 3)(), (_i64 * 3)()
+    _check(_lib.repro_dot_table(fold, dtype, off, cnt), "repro_dot_table")
+    base = _aligned_ptr(workspace)[0] - workspace.data_ptr()
+    return tuple(workspace[base + o: base + o + c * sz].view(dt)
+                 for o, c, dt, sz in zip(off, cnt, (torch.int32, torch.int32, torch.int64), (4, 4, 8)))
+
+
+def dot_deposit_async(x, y, fold: int, workspace, stream=None):
+    dt = _dtype_code(x)
+    if y is not None and y.numel() != x.numel():
+        raise ValueError("x and y differ in length")
+    wp, wb = _aligned_ptr(workspace)
+    _check(_lib.repro_dot_deposit_async(_dev(x, "x"), None if y is None else _dev(y, "y", x.dtype), x.numel(),
+                                        fold, dt, wp, wb, _stream_ptr(stream)), "repro_dot_deposit_async")
+
+
+def dot_finish_async(fold: int, dtype: int, out, workspace, status, stream=None):
+    torch = _torch()
+    wp, wb = _aligned_ptr(workspace)
+    _check(_lib.repro_dot_finish_async(fold, dtype, _dev(out, "out"), wp, wb, _stream_ptr(stream),
+                                       _dev(status, "status", torch.int32)), "repro_dot_finish_async")
     return out
 
 

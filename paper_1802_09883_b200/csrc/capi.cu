@@ -706,23 +706,28 @@ size_t repro_dot_workspace_bytes(int32_t fold, int32_t dtype) {
 
 namespace {
 
+// phase: 3 = whole call; 1 = zero + deposit (multi-GPU split form); 2 = fold
+// + Eq. 1 only (after the slot tables were all-reduced)
 int enqueue_array(const void *x, const void *y, int64_t n, int32_t K, int32_t dt, void *out, void *ws,
-                  cudaStream_t st, uint32_t **flags_out) {
+                  cudaStream_t st, uint32_t **flags_out, int phase = 3) {
     OnchipWs w = carve_onchip(ws, n, 1, K, dt);
     *flags_out = w.flags;
     t_path = 0;
-    if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
-    // register-state kernel (k_array.cu) for 16-byte aligned arrays; the
-    // keyless on-chip kernel otherwise (or when a kernel variant is forced)
-    const bool aligned = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
-    int rc = (aligned && onchip_variant() == 0)
+    if (phase & 1) {
+        if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
+        // register-state kernel (k_array.cu) for 16-byte aligned arrays; the
+        // keyless on-chip kernel otherwise (or when a kernel variant is forced)
+        const bool aligned = (((uintptr_t)x | (uintptr_t)y) & 15) == 0;
+        int rc = (aligned && onchip_variant() == 0)
                  ? timed("rsum", st, [&] {
                        return launch_rsum(dt, K, x, y, n, w.kglob, w.slots, w.flags, st, &t_launches);
                    })
                  : timed("onchip_accumulate", st, [&] {
                        return launch_onchip_array(dt, K, x, y, n, w.kglob, w.slots, w.flags, st, &t_launches);
                    });
-    if (rc) return map_launch(rc);
+        if (rc) return map_launch(rc);
+    }
+    if (!(phase & 2)) return REPRO_OK;
     return map_launch(timed("fold", st, [&] {
         return launch_fold(dt, K, 1, w.kglob, w.slots, 0, nullptr, nullptr, nullptr, out, w.flags, st,
                            &t_launches);
@@ -759,6 +764,41 @@ int repro_dot_async(const void *x, const void *y, int64_t n, int32_t fold, int32
     cudaStream_t st = (cudaStream_t)stream;
     uint32_t *flags = nullptr;
     int rc = enqueue_array(x, y, n, fold, dtype, out, workspace, st, &flags);
+    if (rc != REPRO_OK) return rc;
+    return map_launch(timed("status", st, [&] { return launch_status(flags, d_status, st, &t_launches); }));
+}
+
+int repro_dot_table(int32_t fold, int32_t dtype, int64_t *offsets, int64_t *counts) {
+    if (!valid_shape(1, fold, dtype) || !offsets || !counts) return REPRO_EINVAL;
+    OnchipWs w = carve_onchip(nullptr, 0, 1, fold, dtype);
+    offsets[0] = (int64_t)(uintptr_t)w.flags;
+    offsets[1] = (int64_t)(uintptr_t)w.kglob;
+    offsets[2] = (int64_t)(uintptr_t)w.slots;
+    counts[0] = 1;
+    counts[1] = 1;
+    counts[2] = (int64_t)slot_count(dtype, fold) * 2;
+    return REPRO_OK;
+}
+
+int repro_dot_deposit_async(const void *x, const void *y, int64_t n, int32_t fold, int32_t dtype, void *workspace,
+                            size_t ws_bytes, void *stream) {
+    t_launches = 0;
+    if (n < 0 || !valid_shape(1, fold, dtype) || !workspace || (n > 0 && !x)) return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    if (ws_bytes < repro_dot_workspace_bytes(fold, dtype)) return REPRO_ENOMEM;
+    uint32_t *flags = nullptr;
+    return enqueue_array(x, y, n, fold, dtype, nullptr, workspace, (cudaStream_t)stream, &flags, 1);
+}
+
+int repro_dot_finish_async(int32_t fold, int32_t dtype, void *out, void *workspace, size_t ws_bytes, void *stream,
+                           int32_t *d_status) {
+    t_launches = 0;
+    if (!valid_shape(1, fold, dtype) || !out || !workspace || !d_status) return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    if (ws_bytes < repro_dot_workspace_bytes(fold, dtype)) return REPRO_ENOMEM;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *flags = nullptr;
+    int rc = enqueue_array(nullptr, nullptr, 0, fold, dtype, out, workspace, st, &flags, 2);
     if (rc != REPRO_OK) return rc;
     return map_launch(timed("status", st, [&] { return launch_status(flags, d_status, st, &t_launches); }));
 }

@@ -37,6 +37,9 @@ namespace repro {
 #ifndef ONCHIP_NB
 #define ONCHIP_NB 4
 #endif
+#ifndef ONCHIP_PRED
+#define ONCHIP_PRED 0  // 1: lanes whose limb is zero skip the atomic (predicated, no branch)
+#endif
 
 // Table geometry.  The limb counters are WORD-MAJOR: counter w of group g is
 // cnt[w * GQ + g], with GQ the group count rounded up to a multiple of 4 (1024
@@ -164,6 +167,12 @@ __device__ __forceinline__ void row_limbs(typename Fmt<DT>::V s, uint32_t (&lo)[
 __device__ __forceinline__ void red_shared(uint32_t a, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
 }
+// the same, predicated off for a zero addend (a lane that adds nothing does
+// not take part in the bank access)
+__device__ __forceinline__ void red_shared_nz(uint32_t a, uint32_t v) {
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}"
+                 :: "r"(a), "r"(v) : "memory");
+}
 
 // Generic deposit of one row: digits under the window whose scale is already
 // applied to s; key < 0 deposits nothing.  UNIFORM (small G): a warp whose
@@ -281,10 +290,17 @@ __device__ __forceinline__ void deposit_batch(uint32_t cbase, uint32_t kstride, 
             uint32_t any = 0;
 #pragma unroll
             for (int i = 0; i < NB; ++i) any |= h ? hi[i][l] : lo[i][l];
-            if (ONCHIP_SKIPZ == 0 || __any_sync(0xffffffffu, any != 0u)) {
+            if (ONCHIP_PRED == 1) {
                 const uint32_t off = (uint32_t)(Cfg::LIMBS * l + h) * wstride;
 #pragma unroll
-                for (int i = 0; i < NB; ++i) red_shared(a[i] + off, h ? hi[i][l] : lo[i][l]);
+                for (int i = 0; i < NB; ++i) red_shared_nz(a[i] + off, h ? hi[i][l] : lo[i][l]);
+            } else if (ONCHIP_SKIPZ == 0 || __any_sync(0xffffffffu, any != 0u)) {
+                const uint32_t off = (uint32_t)(Cfg::LIMBS * l + h) * wstride;
+#pragma unroll
+                for (int i = 0; i < NB; ++i) {
+                    if (ONCHIP_PRED == 2) red_shared_nz(a[i] + off, h ? hi[i][l] : lo[i][l]);
+                    else red_shared(a[i] + off, h ? hi[i][l] : lo[i][l]);
+                }
             }
         }
     }

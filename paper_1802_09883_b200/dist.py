@@ -59,6 +59,18 @@ def groupby_sum_multi_dist(R, keys, cols, n_groups, fold, proj, outs, counts, wo
     return outs
 
 
+def dot_dist(R, x, y, fold, out, workspace, status, group=None, stream=None):
+    """Single-array SUM (y None) or dot product over the elements of all
+    ranks: deposit the local shard, all-reduce the slot table, read out on
+    every rank (same bits as one GPU over the concatenated arrays)."""
+    dt = R.F64 if x.dtype == torch.float64 else R.F32
+    R.dot_deposit_async(x, y, fold, workspace, stream)
+    flags, kglob, slots = R.dot_table_views(workspace, fold, dt)
+    allreduce_table(flags, kglob, slots, group)
+    R.dot_finish_async(fold, dt, out, workspace, status, stream)
+    return out
+
+
 def shard_rows(n: int, world: int, rank: int):
     """Contiguous row range [r0, r1) of `rank` (rows are independent units)."""
     r0 = n * rank // world

@@ -164,3 +164,36 @@ def test_full_size_sum(R):
     got = R.dot(dev(x), dev(y), 3)
     rc, ref = O.dot(x, y, 3)
     assert rc == O.OK and same(got, ref)
+
+
+@pytest.mark.parametrize("ranks", [2, 3, 8])
+def test_split_form_emulated_ranks(R, ranks):
+    """The multi-GPU split form: each emulated rank deposits its shard into
+    its own workspace; the slot tables are combined with the integer
+    reductions dist.allreduce_table performs (OR / MAX / SUM) and read out --
+    the same bits as one call over the whole array."""
+    n = 1000003
+    x = values(n, np.float64, 21)
+    y = values(n, np.float64, 22)
+    x[n // 3] = 2.0 ** 60  # one rank sees a higher window top than the others
+    dx, dy = dev(x), dev(y)
+    for yy, ref in ((None, O.rsum(x, 3)[1]), (dy, O.dot(x, y, 3)[1])):
+        tables = []
+        wss = []
+        for r in range(ranks):
+            a, b = n * r // ranks, n * (r + 1) // ranks
+            ws = R.make_dot_workspace(3, R.F64)
+            R.dot_deposit_async(dx[a:b], None if yy is None else yy[a:b], 3, ws)
+            wss.append(ws)
+            tables.append(R.dot_table_views(ws, 3, R.F64))
+        f0, k0, s0 = tables[0]
+        for f, k, s in tables[1:]:
+            f0.copy_(f0 | f)
+            k0.copy_(torch.maximum(k0, k))
+            s0.add_(s)
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+        status = torch.zeros(1, dtype=torch.int32, device="cuda")
+        R.dot_finish_async(3, R.F64, out, wss[0], status)
+        torch.cuda.synchronize()
+        assert status.item() == 0
+        assert same(out, ref)
