@@ -254,6 +254,41 @@ int repro_dot_finish_async(int32_t fold, int32_t dtype, void *out,
                            int32_t *d_status);
 
 /* ------------------------------------------------------------------------
+ * Runtime path / depth selection (the paper picks the
+ * partitioning depth offline and names adaptive selection, PAPER.md:
+ * 1155-1176).  Every path and depth returns the same bits, so these settings
+ * change speed only.  They are process-wide (not thread-safe against
+ * concurrent calls) and take effect at the next call; workspace sizes
+ * (repro_*_workspace_bytes) must be re-queried after a change, since the
+ * on-chip and partitioned paths need different workspaces (a workspace too
+ * small for the chosen path gives REPRO_ENOMEM, never a wrong result).
+ * ---------------------------------------------------------------------- */
+
+/* Current settings for (fold, dtype): the group count up to which the
+ * on-chip path is used (0 = up to its capacity, repro_onchip_max_groups)
+ * and the widest partition id (bits) scattered in ONE pass (wider ids take
+ * two passes).  Either output pointer may be NULL.  Host-only call. */
+int repro_tune_get(int32_t fold, int32_t dtype,
+                   int32_t *onchip_max_groups_out, int32_t *onepass_bits_out);
+
+/* Set them: onchip_max_groups >= 0 (0 = capacity; values above the capacity
+ * act as the capacity), onepass_bits in 1..10 (0 = leave unchanged).
+ * REPRO_EINVAL otherwise.  Host-only call. */
+int repro_tune_set(int32_t fold, int32_t dtype, int32_t onchip_max_groups,
+                   int32_t onepass_bits);
+
+/* Measure the crossovers on this GPU and set them: (1) the largest group
+ * count (powers of two from 2048 up to the on-chip capacity) at which the
+ * on-chip path is not slower than the partitioned one, (2) the largest
+ * partition-id width (2..10 bits) at which one scatter pass is not slower
+ * than two.  Inputs are n (clamped to [2^16, 2^27]) device-generated rows
+ * shaped like BASELINE config 2 (uniform keys, values in [-1, 1)).
+ * Blocking; allocates and frees its own device memory.  Outputs may be
+ * NULL.  REPRO_EINVAL for n < 2^16 or a bad fold / dtype. */
+int repro_autotune(int64_t n, int32_t fold, int32_t dtype,
+                   int32_t *onchip_max_groups_out, int32_t *onepass_bits_out);
+
+/* ------------------------------------------------------------------------
  * Accumulator handles: n_groups device-resident repro<ScalarT, fold> states
  * (the paper's intermediate aggregates).  A handle is not
  * thread-safe; distinct handles are independent.  All calls are blocking.

@@ -68,6 +68,9 @@ _sig("repro_dot_async", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _sz,
 _sig("repro_dot_table", ctypes.c_int, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64))
 _sig("repro_dot_deposit_async", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _vp, _sz, _vp)
 _sig("repro_dot_finish_async", ctypes.c_int, _i32, _i32, _vp, _vp, _sz, _vp, _vp)
+_sig("repro_tune_get", ctypes.c_int, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32))
+_sig("repro_tune_set", ctypes.c_int, _i32, _i32, _i32, _i32)
+_sig("repro_autotune", ctypes.c_int, _i64, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32))
 _sig("repro_acc_create", ctypes.c_int, ctypes.POINTER(_vp), _i32, _i32, _i32)
 _sig("repro_acc_deposit", ctypes.c_int, _vp, _vp, _vp, _i64)
 _sig("repro_acc_merge", ctypes.c_int, _vp, _vp)
@@ -344,6 +347,25 @@ def dot_finish_async(fold: int, dtype: int, out, workspace, status, stream=None)
     _check(_lib.repro_dot_finish_async(fold, dtype, _dev(out, "out"), wp, wb, _stream_ptr(stream),
                                        _dev(status, "status", torch.int32)), "repro_dot_finish_async")
     return out
+
+
+def tune_get(fold: int, dtype: int) -> dict:
+    """Path / depth settings (repro_tune_get): on-chip crossover (0 =
+    capacity) and the widest one-pass partition id in bits."""
+    a, b = _i32(), _i32()
+    _check(_lib.repro_tune_get(fold, dtype, ctypes.byref(a), ctypes.byref(b)), "repro_tune_get")
+    return {"onchip_max_groups": a.value, "onepass_bits": b.value}
+
+
+def tune_set(fold: int, dtype: int, onchip_max_groups: int = 0, onepass_bits: int = 0):
+    _check(_lib.repro_tune_set(fold, dtype, onchip_max_groups, onepass_bits), "repro_tune_set")
+
+
+def autotune(n: int = 1 << 26, fold: int = 3, dtype: int = F64) -> dict:
+    """Measure and set the crossovers on this GPU (repro_autotune)."""
+    a, b = _i32(), _i32()
+    _check(_lib.repro_autotune(n, fold, dtype, ctypes.byref(a), ctypes.byref(b)), "repro_autotune")
+    return {"onchip_max_groups": a.value, "onepass_bits": b.value}
 
 
 def multi_workspace_bytes(n: int, n_groups: int, ncols: int, proj: int, fold: int, dtype: int) -> int:

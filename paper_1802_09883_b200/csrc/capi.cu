@@ -2,6 +2,7 @@
 // argument validation, path choice (on-chip tables vs radix partitioning),
 // workspace layout, launches, device status word.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -42,6 +43,9 @@ namespace {
 thread_local int32_t t_launches = 0;
 thread_local int32_t t_path = -1;
 int32_t g_path_override = -1;
+// f3: group count up to which the
+// on-chip path is used, per [dtype][fold] (0 = its capacity); see repro_autotune
+int32_t g_onchip_cross[2][5] = {};
 
 // ---- per-kernel event timing (repro_timing_enable / _collect) -------------
 struct TimingRec {
@@ -117,7 +121,9 @@ bool valid_shape(int32_t G, int32_t K, int32_t dt) {
 
 // 0 = on-chip, 1 = partitioned, -1 = not supported
 int choose_path(int32_t G, int32_t K, int32_t dt) {
-    const int onchip = onchip_max_groups(K, dt);
+    int onchip = onchip_max_groups(K, dt);
+    const int32_t cross = g_onchip_cross[dt == REPRO_F64][K];
+    if (cross > 0 && g_path_override < 0) onchip = std::min<int>(onchip, cross);
     if (g_path_override == 0) return G <= onchip ? 0 : -1;
     if (g_path_override == 1) return G <= partition_max_groups(K, dt) ? 1 : -1;
     if (G <= onchip) return 0;
@@ -813,6 +819,148 @@ int repro_dot(const void *x, const void *y, int64_t n, int32_t fold, int32_t dty
         return REPRO_EINVAL;
     }
     return array_blocking(x, y, n, fold, dtype, out);
+}
+
+// ---- f3: runtime path / depth selection -----------------------------------
+
+int repro_tune_get(int32_t fold, int32_t dtype, int32_t *onchip_max_groups_out, int32_t *onepass_bits_out) {
+    if (fold < 1 || fold > 4 || (dtype != REPRO_F32 && dtype != REPRO_F64)) return REPRO_EINVAL;
+    if (onchip_max_groups_out) onchip_max_groups_out[0] = g_onchip_cross[dtype == REPRO_F64][fold];
+    if (onepass_bits_out) onepass_bits_out[0] = partition_onepass_bits(dtype == REPRO_F64 ? 1 : 0);
+    return REPRO_OK;
+}
+
+int repro_tune_set(int32_t fold, int32_t dtype, int32_t onchip_max_groups, int32_t onepass_bits) {
+    if (fold < 1 || fold > 4 || (dtype != REPRO_F32 && dtype != REPRO_F64)) return REPRO_EINVAL;
+    if (onchip_max_groups < 0 || onepass_bits < 0) return REPRO_EINVAL;
+    if (onepass_bits > 0 && set_partition_onepass_bits(dtype == REPRO_F64 ? 1 : 0, onepass_bits) != 0)
+        return REPRO_EINVAL;
+    g_onchip_cross[dtype == REPRO_F64][fold] = onchip_max_groups;
+    return REPRO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+__global__ void k_to_f32(const double *__restrict__ a, float *__restrict__ b, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        b[i] = (float)a[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+int repro_autotune(int64_t n, int32_t fold, int32_t dtype, int32_t *onchip_max_groups_out,
+                   int32_t *onepass_bits_out) {
+    if (n < (1 << 16) || !valid_shape(1, fold, dtype)) return REPRO_EINVAL;
+    n = std::min<int64_t>(n, 1ll << 27);
+    const int dt1 = dtype == REPRO_F64 ? 1 : 0;
+    const size_t vsz = dtype == REPRO_F64 ? 8 : 4;
+    const int cap = onchip_max_groups(fold, dtype);
+    const int32_t gmax = std::min<int32_t>(partition_max_groups(fold, dtype), 1 << 20);
+    std::lock_guard<std::mutex> lock(g_cache.mu);
+    // inputs: config-2 rows (uniform keys, values U[-1,1)) regenerated per G
+    int32_t *keys = nullptr;
+    double *v64 = nullptr;
+    void *vals = nullptr, *out = nullptr, *ws = nullptr;
+    size_t wsb = 0;
+    for (int32_t G = 2048; G <= gmax; G *= 2)
+        wsb = std::max(wsb, std::max(ws_bytes_for(0, n, std::min(G, cap), fold, dtype),
+                                     ws_bytes_for(1, n, G, fold, dtype)));
+    bool ok = cudaMalloc(&keys, 4 * (size_t)n) == cudaSuccess && cudaMalloc(&v64, 8 * (size_t)n) == cudaSuccess &&
+              cudaMalloc(&out, vsz * (size_t)gmax) == cudaSuccess && cudaMalloc(&ws, wsb) == cudaSuccess;
+    if (ok && dtype == REPRO_F32) ok = cudaMalloc(&vals, 4 * (size_t)n) == cudaSuccess;
+    if (dtype == REPRO_F64) vals = v64;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ok) ok = cudaEventCreate(&e0) == cudaSuccess && cudaEventCreate(&e1) == cudaSuccess;
+    const int32_t saved_override = g_path_override;
+    const int saved_bits = partition_onepass_bits(dt1);
+    auto gen = [&](int32_t G) {
+        void *cols[1] = {v64};
+        if (launch_synth(2, 0x1802098830ull + 2, 0, n, G, keys, cols, 0) != 0) return false;
+        if (dtype == REPRO_F32) k_to_f32<<<4 * device_props().sms, 256>>>(v64, (float *)vals, n);
+        return cudaStreamSynchronize(0) == cudaSuccess;
+    };
+    auto time_path = [&](int32_t G, int path) -> double {  // best of 3, ms; < 0 on error
+        g_path_override = path;
+        double best = -1;
+        for (int r = 0; r < 4; ++r) {
+            uint32_t *flags = nullptr;
+            cudaEventRecord(e0, 0);
+            const int rc = enqueue_groupby(keys, vals, n, G, fold, dtype, out, 0, nullptr, nullptr, nullptr, ws,
+                                           wsb, 0, &flags);
+            cudaEventRecord(e1, 0);
+            if (rc != REPRO_OK || cudaEventSynchronize(e1) != cudaSuccess) return -1;
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            if (r > 0 && (best < 0 || ms < best)) best = ms;
+        }
+        return best;
+    };
+    int32_t cross = 1024;
+    int bits = saved_bits;
+    const bool tlog = getenv("REPRO_TUNE_LOG") != nullptr;
+    if (ok) {
+        // (1) on-chip vs partitioned crossover above the register-table size
+        bool onchip_wins = true;
+        for (int32_t G = 2048; G <= cap && onchip_wins; G *= 2) {
+            if (!gen(G)) { ok = false; break; }
+            const double a = time_path(G, 0), b = time_path(G, 1);
+            if (tlog) fprintf(stderr, "repro_autotune: G=%d on-chip %.3f ms, partitioned %.3f ms\n", G, a, b);
+            if (a < 0 || b < 0) { ok = false; break; }
+            onchip_wins = a <= b;
+            if (onchip_wins) cross = G;
+        }
+        if (onchip_wins && ok) cross = cap;
+        // (2) one vs two scatter passes, partition-id bits 2 .. 10: the
+        // threshold T minimising sum_b (b <= T ? one(b) : two(b))
+        double one[11] = {}, two[11] = {};
+        int bmax = 1;
+        for (int b = 2; b <= 10 && ok; ++b) {
+            const int64_t G = (int64_t)1024 << b;
+            if (G > gmax) break;
+            if (!gen((int32_t)G)) { ok = false; break; }
+            g_path_override = 1;
+            set_partition_onepass_bits(dt1, b);
+            one[b] = time_path((int32_t)G, 1);
+            set_partition_onepass_bits(dt1, b - 1);
+            two[b] = time_path((int32_t)G, 1);
+            if (tlog)
+                fprintf(stderr, "repro_autotune: G=%lld %d-bit ids: one pass %.3f ms, two passes %.3f ms\n",
+                        (long long)G, b, one[b], two[b]);
+            if (one[b] < 0 || two[b] < 0) { ok = false; break; }
+            bmax = b;
+        }
+        double best = -1;
+        for (int T = 1; T <= bmax && ok; ++T) {
+            double c = 0;
+            for (int b = 2; b <= bmax; ++b) c += b <= T ? one[b] : two[b];
+            if (best < 0 || c < best) {
+                best = c;
+                bits = T;
+            }
+        }
+        if (bmax < 10 && bits == bmax) bits = saved_bits > bmax ? saved_bits : bits;  // untested widths keep theirs
+    }
+    g_path_override = saved_override;
+    set_partition_onepass_bits(dt1, ok ? std::max(bits, 1) : saved_bits);
+    if (ok) g_onchip_cross[dt1][fold] = cross;
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(keys);
+    cudaFree(v64);
+    if (dtype == REPRO_F32) cudaFree(vals);
+    cudaFree(out);
+    cudaFree(ws);
+    if (!ok) {
+        cudaGetLastError();
+        return REPRO_ECUDA;
+    }
+    if (onchip_max_groups_out) onchip_max_groups_out[0] = cross;
+    if (onepass_bits_out) onepass_bits_out[0] = partition_onepass_bits(dt1);
+    return REPRO_OK;
 }
 
 void repro_release_cache(void) {

@@ -101,6 +101,8 @@ void trace_end(int token, const char *name, cudaStream_t st);
 
 // ---- partitioned (high-cardinality) path --------------------------------
 int partition_max_groups(int K, int DT);
+int partition_onepass_bits(int DT);             // f3: partitioning depth setting
+int set_partition_onepass_bits(int DT, int bits);
 size_t partition_workspace_bytes(int64_t n, int32_t G, int K, int DT);
 int launch_partitioned(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
                        void *ws, size_t ws_bytes, int merge, int32_t *acc_k, int64_t *acc_C,

@@ -48,10 +48,10 @@ constexpr int SEG_RT = 8;                    // rows per thread per scatter tile
 #define SEG_RTH 32                           // keys per thread in flight in the histogram
 #endif
 #ifndef PART_HEAVY
-#define PART_HEAVY 1                         // sum a partition with >= n/4 of the rows in place
+#define PART_HEAVY 1                         // sum a partition with >= n/2 of the rows in place
 #endif
 #ifndef SEG_ONEPASS_BITS64
-#define SEG_ONEPASS_BITS64 8                 // binary64 rows: one pass up to 2^this partitions
+#define SEG_ONEPASS_BITS64 9                 // binary64 rows: one pass up to 2^this partitions (wide above 2^8)
 #endif
 #ifndef SEG_ONEPASS_BITS32
 #define SEG_ONEPASS_BITS32 10                // binary32 rows (wide scatter above 2^8)
@@ -88,13 +88,26 @@ struct Plan {
     int hb;          // work items of a heavy partition summed in place
 };
 
-Plan make_plan(int64_t n, int32_t G, int DT) {
+// Partitioning depth (f3 of SURVEY.md 8(f)): partition
+// ids of up to g_onepass_bits[DT] bits are scattered in one pass, wider ones
+// in two.  Defaults from the measured crossovers; settable at run
+// time (repro_tune_set) and measured by repro_autotune.
+int g_onepass_bits[2] = {SEG_ONEPASS_BITS32, SEG_ONEPASS_BITS64};
+constexpr int SEG_ONEPASS_MAX = 10;  // the wide scatter's digit limit
+
+
+// passes: 0 = by the depth setting, 1 / 2 = forced (workspace sizing)
+Plan make_plan(int64_t n, int32_t G, int DT, int passes = 0) {
     Plan pl;
     pl.P = (int)(((int64_t)G + PART_GP - 1) >> PART_LOG_GP);
     pl.pbits = 0;
     while ((1 << pl.pbits) < pl.P) ++pl.pbits;
     pl.Pf = 1 << pl.pbits;
-    if (pl.pbits <= (DT == 1 ? SEG_ONEPASS_BITS64 : SEG_ONEPASS_BITS32)) {
+    bool one = pl.pbits <= g_onepass_bits[DT == 1];
+    if (passes == 1) one = pl.pbits <= SEG_ONEPASS_MAX;
+    if (passes == 2) one = pl.pbits < 2;
+    if (pl.pbits > 2 * SEG_MAX_BITS) one = false;
+    if (one) {
         pl.passes = 1;
         pl.bits[0] = pl.pbits;
         pl.shift[0] = PART_LOG_GP;
@@ -315,11 +328,13 @@ __global__ void __launch_bounds__(256) k_seg_scan(uint32_t *hist, const int32_t 
 
 // single block: base[] = exclusive scan of ptot, pitem[] = exclusive scan of
 // the items per partition, then the item table.  heavy_ok (last pass of a
-// one-pass plan, n >= 2^20): a partition holding >= n/4 of the rows (the
+// one-pass plan, n >= 2^20): a partition holding >= n/2 of the rows (the
 // heaviest; ties: lowest id) is not scattered -- its rows keep no space in the
 // output (ctrl[2] = its id, the scatter skips them) and it gets HB items over
 // the ORIGINAL row range [0, n), which k_part_accumulate reads through a
-// partition filter (skewed keys: the hot partition is summed in place)
+// partition filter (skewed keys: the hot partition is summed in place).
+// Break-even: scattering a partition costs a write and a re-read of its rows
+// (2 n_h row bytes), the in-place sum re-reads the whole input (n row bytes).
 __global__ void __launch_bounds__(1024) k_part_plan(const int64_t *ptot, int P, int64_t chunk_rows, int64_t *base,
                                                     int64_t *pitem, int64_t *items, int32_t *iown, int32_t *ctrl,
                                                     int heavy_ok, int64_t n, int hb) {
@@ -338,7 +353,7 @@ __global__ void __launch_bounds__(1024) k_part_plan(const int64_t *ptot, int P, 
     }
     __syncthreads();
     int heavy = -1;
-    if (heavy_ok && (int64_t)(s_best >> 20) * 4 >= n) heavy = (1 << 20) - 1 - (int)(s_best & ((1u << 20) - 1));
+    if (heavy_ok && (int64_t)(s_best >> 20) * 2 >= n) heavy = (1 << 20) - 1 - (int)(s_best & ((1u << 20) - 1));
     auto rows_of = [&](int p) { return p == heavy ? (int64_t)0 : ptot[p]; };
     auto items_of = [&](int p) { return p == heavy ? (int64_t)hb : (ptot[p] + chunk_rows - 1) / chunk_rows; };
     int64_t rows = 0, its = 0;
@@ -844,9 +859,23 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
 // at most two passes of <= 2^8 digits: 2^16 partitions of 1024 groups
 int partition_max_groups(int, int) { return 1 << (2 * SEG_MAX_BITS + PART_LOG_GP); }
 
+int partition_onepass_bits(int DT) { return g_onepass_bits[DT == 1]; }
+int set_partition_onepass_bits(int DT, int bits) {
+    if (bits < 1 || bits > SEG_ONEPASS_MAX) return -1;
+    g_onepass_bits[DT == 1] = bits;
+    return 0;
+}
+
+// sized for both depths where both are possible, so that a depth change
+// (repro_tune_set / repro_autotune) never outgrows a caller's workspace
 size_t partition_workspace_bytes(int64_t n, int32_t G, int K, int DT) {
-    const Plan pl = make_plan(n, G, DT);
-    return carve(nullptr, n, G, K, DT, pl).bytes;
+    size_t b = carve(nullptr, n, G, K, DT, make_plan(n, G, DT)).bytes;
+    for (int p = 1; p <= 2; ++p) {
+        const Plan pl = make_plan(n, G, DT, p);
+        if (pl.passes == 1 && pl.pbits > SEG_ONEPASS_MAX) continue;
+        b = std::max(b, carve(nullptr, n, G, K, DT, pl).bytes);
+    }
+    return b;
 }
 
 int launch_partitioned(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G, void *ws,

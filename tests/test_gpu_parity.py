@@ -446,7 +446,7 @@ def test_partitioned_errors(R, partitioned):
 @pytest.mark.parametrize("dtype,K,G,n", [(np.float64, 3, 1 << 16, (1 << 21) + 3), (np.float32, 2, 1 << 20, 1 << 22),
                                          (np.float64, 2, 5000, 1 << 20)])
 def test_partitioned_heavy_partition_summed_in_place(R, dtype, K, G, n):
-    # Zipf keys: partition 0 holds far more than n/4 of the rows, so the plan
+    # Zipf keys: partition 0 holds more than n/2 of the rows, so the plan
     # sums it in place from the original columns instead of scattering it
     keys, _ = synth.generate_chunked(3, n, G)
     rng = np.random.default_rng(G)
