@@ -40,6 +40,9 @@ namespace repro {
 #ifndef ONCHIP_PRED
 #define ONCHIP_PRED 0  // 1: lanes whose limb is zero skip the atomic (predicated, no branch)
 #endif
+#ifndef ONCHIP_DYNFOLD
+#define ONCHIP_DYNFOLD 1  // 1: fast-path atomics return the old counter; fold only when one nears 2^30
+#endif
 
 // Table geometry.  The limb counters are WORD-MAJOR: counter w of group g is
 // cnt[w * GQ + g], with GQ the group count rounded up to a multiple of 4 (1024
@@ -167,6 +170,14 @@ __device__ __forceinline__ void row_limbs(typename Fmt<DT>::V s, uint32_t (&lo)[
 __device__ __forceinline__ void red_shared(uint32_t a, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" :: "r"(a), "r"(v) : "memory");
 }
+// the same, returning the counter's old value folded into `big`: bit 31 of
+// big is set once any observed counter has |old| >= 2^30 (bits 31 and 30
+// differ), the trigger of the dynamic fold (ONCHIP_DYNFOLD)
+__device__ __forceinline__ void red_shared_obs(uint32_t a, uint32_t v, uint32_t &big) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+    big |= old ^ (old << 1);
+}
 // the same, predicated off for a zero addend (a lane that adds nothing does
 // not take part in the bank access)
 __device__ __forceinline__ void red_shared_nz(uint32_t a, uint32_t v) {
@@ -177,8 +188,9 @@ __device__ __forceinline__ void red_shared_nz(uint32_t a, uint32_t v) {
 // Generic deposit of one row: digits under the window whose scale is already
 // applied to s; key < 0 deposits nothing.  UNIFORM (small G): a warp whose
 // lanes all hold one group reduces with REDUX first.
-template <int DT, int K, bool UNIFORM>
-__device__ __forceinline__ void deposit_row(uint32_t *cnt, int gq, int key, typename Fmt<DT>::V s, int lane) {
+template <int DT, int K, bool UNIFORM, bool OBS = false>
+__device__ __forceinline__ void deposit_row(uint32_t *cnt, int gq, int key, typename Fmt<DT>::V s, int lane,
+                                            uint32_t *big = nullptr) {
     using Cfg = OnchipCfg<DT, K>;
     uint32_t lo[K], hi[K];
     row_limbs<DT, K>(s, lo, hi);
@@ -206,11 +218,12 @@ __device__ __forceinline__ void deposit_row(uint32_t *cnt, int gq, int key, type
         uint32_t *p = cnt + key;
 #pragma unroll
         for (int l = 0; l < K; ++l) {
-            if (Cfg::LIMBS == 2) {
-                atomicAdd(p + (size_t)(2 * l) * gq, lo[l]);
-                atomicAdd(p + (size_t)(2 * l + 1) * gq, hi[l]);
-            } else {
-                atomicAdd(p + (size_t)l * gq, lo[l]);
+#pragma unroll
+            for (int h = 0; h < Cfg::LIMBS; ++h) {
+                uint32_t *c = p + (size_t)(Cfg::LIMBS * l + h) * gq;
+                const uint32_t v = h ? hi[l] : lo[l];
+                if (OBS) red_shared_obs((uint32_t)__cvta_generic_to_shared(c), v, *big);
+                else atomicAdd(c, v);
             }
         }
     }
@@ -251,9 +264,10 @@ struct Extractors {
 // holds zeros there (one vote per position and batch: small digits and values
 // with few significant bits leave whole counters untouched).  Counter w of
 // group g lives at shared address cbase + g * kstride + w * wstride.
-template <int DT, int K, int NB>
+template <int DT, int K, int NB, bool OBS>
 __device__ __forceinline__ void deposit_batch(uint32_t cbase, uint32_t kstride, uint32_t wstride, const int32_t *key,
-                                              const typename Fmt<DT>::V *val, const Extractors<DT, K> &ex) {
+                                              const typename Fmt<DT>::V *val, const Extractors<DT, K> &ex,
+                                              uint32_t &big) {
     using Cfg = OnchipCfg<DT, K>;
     uint32_t lo[NB][K], hi[NB][K], a[NB];
 #pragma unroll
@@ -298,7 +312,8 @@ __device__ __forceinline__ void deposit_batch(uint32_t cbase, uint32_t kstride, 
                 const uint32_t off = (uint32_t)(Cfg::LIMBS * l + h) * wstride;
 #pragma unroll
                 for (int i = 0; i < NB; ++i) {
-                    if (ONCHIP_PRED == 2) red_shared_nz(a[i] + off, h ? hi[i][l] : lo[i][l]);
+                    if (OBS) red_shared_obs(a[i] + off, h ? hi[i][l] : lo[i][l], big);
+                    else if (ONCHIP_PRED == 2) red_shared_nz(a[i] + off, h ? hi[i][l] : lo[i][l]);
                     else red_shared(a[i] + off, h ? hi[i][l] : lo[i][l]);
                 }
             }
@@ -667,7 +682,11 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
     };
 
     const bool small_g = G <= ONCHIP_SMALLG;
-    int since = 0;  // rows' worth of digits in the counters since the last fold
+    int since = 0;     // rows' worth of digits in the counters since the last fold
+    uint32_t big = 0;  // dynamic fold: bit 31 = an observed counter had |old| >= 2^30
+    // dynamic fold (not for lane copies: their folds are cheap, and an atomic
+    // that returns its old value costs more than the folds it saves there)
+    const bool dyn = ONCHIP_DYNFOLD && !lanerep;
 
     // a1: coalesced loads (immediate offsets i*TPB from one base pointer),
     // bounds-checked, straight from global memory
@@ -758,6 +777,7 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         // whole block (and orders the previous tile's deposits before a fold).
         if (ONCHIP_FAST && !small_g) {
             int slow = kuni < 0 || rem < TILE - tid;
+            slow |= (int)(big >> 31) << 1;  // bit 1: a counter neared 2^30 (dynamic fold)
             if (!slow) {
                 // k*(b) <= kuni  <=>  |b| < 2^(W kuni + W - 1 - m): compare the
                 // magnitude bits (sign shifted out); NaN/Inf fail it too
@@ -773,24 +793,40 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                 }
                 slow = (hwmax >= lim) | (kmax >= (uint32_t)G);
             }
-            const int any_slow = __syncthreads_or(slow);
+            const int any_flags = __syncthreads_or(slow);
+            const int any_slow = any_flags & 1;
             refill();
             if (!any_slow) {
-                if (since + VTILE > Cfg::LIMIT) {
+                // static cadence: fold every LIMIT rows.  Dynamic (ONCHIP_DYNFOLD,
+                // every deposit returns the counter's old value): fold when a
+                // counter was seen at |old| >= 2^30 in the previous tile; with
+                // at most TILE deposits per counter per tile a counter then
+                // stays below 2^30 + (TILE + 1) 2^19 < 2^31
+                const bool fold_now = dyn ? (any_flags & 2) != 0 : since + VTILE > Cfg::LIMIT;
+                if (fold_now) {
                     fold_all(true);
                     since = 0;
+                    big = 0;
                     __syncthreads();
                 }
-                since += VTILE;
+                if (!dyn) since += VTILE;
                 const Extractors<DT, K> ex(kuni);
                 constexpr int RD = SRC::ONES ? R - RIN : R;  // virtual rows with a digit cascade
                 constexpr int NB = ONCHIP_NB < RD ? ONCHIP_NB : RD;
 #pragma unroll
                 for (int i0 = 0; i0 < RD; i0 += NB) {
-                    if (i0 + NB <= RD) deposit_batch<DT, K, NB>(fbase, kstride, wstride, key + i0, val + i0, ex);
-                    else
-                        deposit_batch<DT, K, (RD % NB ? RD % NB : NB)>(fbase, kstride, wstride, key + i0, val + i0,
-                                                                       ex);
+                    constexpr int NL = RD % NB ? RD % NB : NB;
+                    if (dyn) {
+                        if (i0 + NB <= RD)
+                            deposit_batch<DT, K, NB, true>(fbase, kstride, wstride, key + i0, val + i0, ex, big);
+                        else
+                            deposit_batch<DT, K, NL, true>(fbase, kstride, wstride, key + i0, val + i0, ex, big);
+                    } else {
+                        if (i0 + NB <= RD)
+                            deposit_batch<DT, K, NB, false>(fbase, kstride, wstride, key + i0, val + i0, ex, big);
+                        else
+                            deposit_batch<DT, K, NL, false>(fbase, kstride, wstride, key + i0, val + i0, ex, big);
+                    }
                 }
                 if (SRC::ONES) {
                     // COUNT column: the limbs of 1 under the window kuni, once per tile
@@ -804,8 +840,10 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                             if (c != 0u) {
                                 const uint32_t off = (uint32_t)(Cfg::LIMBS * l + h) * wstride;
 #pragma unroll
-                                for (int i = 0; i < RIN; ++i)  // fast path: every key is valid
-                                    red_shared(fbase + kstride * (uint32_t)key[R - RIN + i] + off, c);
+                                for (int i = 0; i < RIN; ++i) {  // fast path: every key is valid
+                                    if (dyn) red_shared_obs(fbase + kstride * (uint32_t)key[R - RIN + i] + off, c, big);
+                                    else red_shared(fbase + kstride * (uint32_t)key[R - RIN + i] + off, c);
+                                }
                             }
                         }
                     }
@@ -835,8 +873,11 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                 kc[i] = cur;
             }
         }
-        const bool fold = since + VTILE > Cfg::LIMIT;
-        const int any = __syncthreads_or(changed);  // also: previous tile's deposits are done
+        // dynamic mode: every deposit is observed; fold when a counter was
+        // seen at |old| >= 2^30 (bit 1 of the barrier's OR)
+        const int any_flags = __syncthreads_or(changed | (int)(big >> 31) << 1);  // + previous tile done
+        const int any = any_flags & 1;
+        const bool fold = dyn ? (any_flags & 2) != 0 : since + VTILE > Cfg::LIMIT;
         if (!(ONCHIP_FAST && !small_g)) refill();
         if (any || fold) {
             // fold counters into the level sums and demote moved groups
@@ -851,7 +892,10 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                 if (lane == 0) { atomicMin(&kminmax[0], lo); atomicMax(&kminmax[1], hi); }
             }
             __syncthreads();
-            if (fold) since = 0;
+            if (fold) {
+                since = 0;
+                big = 0;
+            }
             if (any) {
                 kuni = kminmax[0] == kminmax[1] ? kminmax[1] : -1;
 #pragma unroll
@@ -871,6 +915,11 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
             for (int i = 0; i < R; ++i)
                 deposit_row<DT, K, false>(cnt + lane, gq, key[i] >= 0 ? 32 * key[i] : -1,
                                           F::mul(val[i], F::pow2(F::m - F::W * kc[i])), lane);
+        } else if (dyn) {
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+                deposit_row<DT, K, false, true>(cnt, gq, key[i], F::mul(val[i], F::pow2(F::m - F::W * kc[i])), lane,
+                                                &big);
         } else if (kuni >= 0) {
             const V scale = F::pow2(F::m - F::W * kuni);
 #pragma unroll

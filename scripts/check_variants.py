@@ -12,9 +12,14 @@ sys.path.insert(0, %r)
 import oracle as O, paper_1802_09883_b200 as R
 from paper_1802_09883_b200 import synth
 res = []
-for cfg, n, G in ((0, 1 << 16, 16), (1, 1 << 22, 1024), (1, 1 << 24, 1024), (1, 1 << 22, 3000)):
+for cfg, n, G in ((0, 1 << 16, 16), (1, 1 << 22, 1024), (1, 1 << 24, 1024), (1, 1 << 22, 3000),
+                  ("hot", 1 << 22, 1024), ("hot", 1 << 22, 16), ("hotneg", 1 << 22, 1024)):
     if cfg == 0:
         k, v = synth.generate(0, n=n)
+    elif cfg in ("hot", "hotneg"):  # every row in one group, same-sign values: counters grow linearly
+        k, v = synth.generate(1, n=n, n_groups=G)
+        k[:] = 7
+        v = np.abs(v) * (1 if cfg == "hot" else -1)
     else:
         k, v = synth.generate(1, n=n, n_groups=G)
     out = R.groupby_sum(torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda(), G, 3).cpu().numpy()
