@@ -41,6 +41,10 @@ int launch_onchip_multi(int DT, int K, int proj, int ncols, const int32_t *keys,
         }                                                                                                     \
         return -1;                                                                                            \
     } while (0)
+    // config-4 shape with a handful of groups: per-thread register state
+    // (k_lean.cu); 1 = not handled there
+    const int lr = launch_lean_multi(DT, K, proj, ncols, keys, cols, n, G, kglob, slots, status, st, launches);
+    if (lr != 1) return lr;
     using C64_1 = SrcCols<1, 1>;
     using C64_2 = SrcCols<1, 2>;
     using C64_4 = SrcCols<1, 4>;

@@ -613,10 +613,24 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         for (int i = tid; i < K * gq; i += TPB) tot[i] = 0;
     for (int i = tid; i < CW * gq; i += TPB) cnt[i] = 0;
     for (int i = tid; i < gq; i += TPB) { ktop_cur[i] = 0; ktop_next[i] = 0; }
+    // COUNT column (SRC::ONES): the limbs of 1 under the uniform window,
+    // recomputed when the window changes (kminmax[2 .. 2 + 2K))
+    uint32_t *climb = reinterpret_cast<uint32_t *>(kminmax + 2);
+    auto set_count_limbs = [&](int k) {
+        if (SRC::ONES && tid == 0) {
+            uint32_t clo[K], chi[K];
+            row_limbs<DT, K>(F::pow2(F::m - F::W * k), clo, chi);
+#pragma unroll
+            for (int l = 0; l < K; ++l) { climb[2 * l] = clo[l]; climb[2 * l + 1] = chi[l]; }
+        }
+    };
+    set_count_limbs(0);
     __syncthreads();
     // block-uniform window top: when every group has the same top `kuni`,
-    // rows need no per-group lookup (the common case after the first tiles)
+    // rows need no per-group lookup (the common case after the first tiles);
+    // the fast path's extractors follow it
     int kuni = 0;
+    Extractors<DT, K> ex(0);
 
     // small G: per-lane counter copies (OnchipCfg::LANE_G); their level sums
     // live in shared memory per counter word, rtot[g][w]
@@ -810,7 +824,6 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                     __syncthreads();
                 }
                 if (!dyn) since += VTILE;
-                const Extractors<DT, K> ex(kuni);
                 constexpr int RD = SRC::ONES ? R - RIN : R;  // virtual rows with a digit cascade
                 constexpr int NB = ONCHIP_NB < RD ? ONCHIP_NB : RD;
 #pragma unroll
@@ -829,14 +842,12 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                     }
                 }
                 if (SRC::ONES) {
-                    // COUNT column: the limbs of 1 under the window kuni, once per tile
-                    uint32_t clo[K], chi[K];
-                    row_limbs<DT, K>(F::pow2(F::m - F::W * kuni), clo, chi);
+                    // COUNT column: the limbs of 1 under the window kuni
 #pragma unroll
                     for (int l = 0; l < K; ++l) {
 #pragma unroll
                         for (int h = 0; h < Cfg::LIMBS; ++h) {
-                            const uint32_t c = h ? chi[l] : clo[l];
+                            const uint32_t c = climb[2 * l + (Cfg::LIMBS == 2 ? h : 0)];
                             if (c != 0u) {
                                 const uint32_t off = (uint32_t)(Cfg::LIMBS * l + h) * wstride;
 #pragma unroll
@@ -898,6 +909,10 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
             }
             if (any) {
                 kuni = kminmax[0] == kminmax[1] ? kminmax[1] : -1;
+                if (kuni >= 0) {
+                    ex = Extractors<DT, K>(kuni);
+                    set_count_limbs(kuni);  // ordered before use by the next tile's barrier
+                }
 #pragma unroll
                 for (int i = 0; i < R; ++i)
                     if (key[i] >= 0) kc[i] = ktop_cur[key[i]];

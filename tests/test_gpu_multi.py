@@ -35,16 +35,64 @@ def check(R, keys, cols, G, K, proj, path=None):
     assert np.array_equal(counts.cpu().numpy(), ref_counts)
 
 
-@pytest.mark.parametrize("n", [1, 1000, 3 * 512 * 7 + 13, 1 << 20])
-def test_config4_shape_fused(R, n):
+@pytest.fixture(params=[0, 1], ids=["lean-kernel", "onchip-kernel"])
+def variant(R, request):
+    """0: config-4 shapes with <= 4 groups take the per-thread register
+    kernel (k_lean.cu); 1: force the shared-memory on-chip kernel."""
+    R.set_kernel_variant(request.param)
+    yield request.param
+    R.set_kernel_variant(0)
+
+
+@pytest.mark.parametrize("n", [1, 1000, 3 * 512 * 7 + 13, 1 << 20, (1 << 22) + 5])
+def test_config4_shape_fused(R, variant, n):
     keys, (qty, price, disc, tax) = synth.generate(4, n=n)
     check(R, keys, [qty, price, disc, tax], 4, 3, 1, path=2)
 
 
-@pytest.mark.parametrize("K", [1, 2, 4])
-def test_config4_shape_other_folds(R, K):
+@pytest.mark.parametrize("K", [1, 2, 3, 4])
+def test_config4_shape_other_folds(R, variant, K):
     keys, cols = synth.generate(4, n=200003)
     check(R, keys, list(cols), 4, K, 1, path=2)
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 4])
+def test_config4_shape_fewer_groups(R, G):
+    keys, cols = synth.generate(4, n=300001, n_groups=G)
+    check(R, keys, list(cols), G, 3, 1, path=2)
+
+
+@pytest.mark.parametrize("where", ["first", "middle", "last"])
+@pytest.mark.parametrize("what", ["other_window", "zero", "tiny"])
+def test_config4_lean_block_fallback(R, where, what):
+    """A value off the block's lattice window (a larger or smaller k*, or a
+    zero) sends that block through the generic code: same bits as the oracle."""
+    n = 1 << 21
+    keys, cols = synth.generate(4, n=n)
+    cols = [c.copy() for c in cols]
+    i = {"first": 0, "middle": n // 2 + 3, "last": n - 1}[where]
+    if what == "other_window":
+        cols[1][i] = 3.0e12  # price beyond 2^27: k* = 2
+    elif what == "zero":
+        cols[0][i] = 0.0     # qty 0: k* = 0 < 1
+    else:
+        cols[1][i] = 1.0e-9  # price below 2^-13: k* = 0
+    check(R, keys, cols, 4, 3, 1, path=2)
+
+
+def test_config4_lean_errors(R):
+    keys, cols = synth.generate(4, n=1 << 20)
+    cols = [c.copy() for c in cols]
+    bad = cols[2].copy()
+    bad[777777] = np.nan
+    with pytest.raises(R.ReproError) as e:
+        R.groupby_sum_multi(dev(keys), [dev(cols[0]), dev(cols[1]), dev(bad), dev(cols[3])], 4, 3, proj=1)
+    assert e.value.status == R.EDOM
+    k2 = keys.copy()
+    k2[5] = 4
+    with pytest.raises(R.ReproError) as e:
+        R.groupby_sum_multi(dev(k2), [dev(c) for c in cols], 4, 3, proj=1)
+    assert e.value.status == R.EKEY
 
 
 @pytest.mark.parametrize("dtype,ncols,G", [(np.float64, 1, 7), (np.float64, 2, 100), (np.float64, 4, 200),
