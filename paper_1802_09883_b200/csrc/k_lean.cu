@@ -38,6 +38,12 @@ namespace {
 
 bool lean_disabled() { return onchip_variant() != 0; }  // variants 1-3 force the on-chip kernel
 
+#ifndef LEAN_PIPE
+#define LEAN_PIPE 1  // prefetch the next quad of rows while depositing this one
+#endif
+#ifndef LEAN_MINB
+#define LEAN_MINB 1  // resident blocks per SM the register budget is sized for
+#endif
 constexpr int LEAN_TPB = 256;  // = OnchipCfg::TPB (the fallback runs accumulate_range)
 constexpr int LEAN_GL = 4;     // groups handled
 constexpr int LEAN_U = 4;      // rows per thread per iteration
@@ -75,7 +81,7 @@ struct LeanGeom {
 };
 
 template <int DT, int K, class SRC>
-__global__ void __launch_bounds__(LEAN_TPB, 2)
+__global__ void __launch_bounds__(LEAN_TPB, LEAN_MINB)
 k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t G, int64_t chunk,
              int32_t *__restrict__ kglob, unsigned long long *__restrict__ slots, uint32_t *__restrict__ status) {
     using F = Fmt<DT>;
@@ -121,27 +127,55 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
     const uint32_t tbase = (uint32_t)__cvta_generic_to_shared(wt) + 4u * (uint32_t)lane;
     const uint32_t cbase = tbase + 4u * 32u * (uint32_t)NPOS;  // COUNT copies
 
-    // fold: sum the 32 lane copies of every position (exact in 32 bits) into
-    // the warp's int64 sums and clear them
+    // fold: sum the 32 lane copies of every position into the warp's int64
+    // sums and clear them.  The counters hold RAW limbs (see take): the sum
+    // of a position is corrected by (rows of its group since the last fold) x
+    // (the limb's constant bias), mod 2^32 -- exact, since the true sum of at
+    // most 32 x 4 x LEAN_FOLD_IT balanced limbs fits an int32.
+    auto copies_sum = [&](int p) {
+        uint4 *c = reinterpret_cast<uint4 *>(wt + (size_t)p * 32);
+        uint32_t s = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int ch = (i + lane) & 7;
+            const uint4 v = c[ch];
+            s += v.x + v.y + v.z + v.w;
+            c[ch] = make_uint4(0u, 0u, 0u, 0u);
+        }
+        return s;
+    };
     auto fold = [&]() {
         __syncwarp();
-        for (int p = lane; p < NPOS + GL; p += 32) {
-            uint4 *c = reinterpret_cast<uint4 *>(wt + (size_t)p * 32);
-            uint32_t s = 0;
+        uint32_t ng = 0;
+        if (lane < GL) {
+            ng = copies_sum(NPOS + lane);
+            wsum[NPOS + lane] += (int64_t)ng;
+        }
+        uint32_t N[GL];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int ch = (i + lane) & 7;
-                const uint4 v = c[ch];
-                s += v.x + v.y + v.z + v.w;
-                c[ch] = make_uint4(0u, 0u, 0u, 0u);
+        for (int g = 0; g < GL; ++g) N[g] = __shfl_sync(0xffffffffu, ng, g);
+        for (int p = lane; p < NPOS; p += 32) {
+            const int g = (p / CW) % GL, w = p % CW;
+            uint32_t bias;
+            if (DT == 1) {
+                bias = (w & 1) ? 0x80000000u : 0x80000u;  // hi: exponent field of E_l; lo: the 2^19 offset
+            } else {
+                const int ue = F::W * (k0 - w) - F::m;  // binary32: one limb per level, bias = bits(E_l)
+                bias = ((uint32_t)(ue + F::m + F::BIAS) << 23) | (1u << 22);
             }
-            wsum[p] += p < NPOS ? (int64_t)(int32_t)s : (int64_t)s;
+            uint32_t nsel = N[0];
+#pragma unroll
+            for (int q = 1; q < GL; ++q) nsel = g == q ? N[q] : nsel;
+            const uint32_t s = copies_sum(p) - bias * nsel;
+            wsum[p] += (int64_t)(int32_t)s;
         }
         __syncwarp();
     };
 
-    // deposit one row: digits of the ND virtual values under k0 as balanced
-    // limbs, one conflict-free atomic per limb, +1 on the group's COUNT copy.
+    // deposit one row: digits of the ND virtual values under k0 as RAW limbs
+    // (the balanced limbs of the on-chip kernel plus a constant per limb,
+    // removed at the fold), one conflict-free atomic per limb, +1 on the
+    // group's COUNT copy.
     // Position (j * GL + g) * CW + w sits at byte 128 * position of the table.
     auto take = [&](int32_t key, const V (&c)[SRC::NCOL], bool &bad) {
         int32_t vk[NV];
@@ -163,13 +197,13 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
                     const double x = __hiloint2double(__double2hiint((double)r), __double2loint((double)r) | 1);
                     const double t = __dadd_rn(x, (double)ex.e[l]);
                     const uint32_t tlo = (uint32_t)__double2loint(t), thi = (uint32_t)__double2hiint(t);
-                    lo = (tlo & 0xFFFFFu) - 0x80000u;
-                    hi = __funnelshift_r(tlo, thi, 20) - ex.eb[l];
+                    lo = tlo & 0xFFFFFu;                 // raw: balanced limb + 2^19
+                    hi = __funnelshift_r(tlo, thi, 20);  // raw: balanced limb + 2^31 (ex.eb[l])
                     if (l + 1 < K) r = (V)__dsub_rn((double)r, __dsub_rn(t, (double)ex.e[l]));
                 } else {
                     const float x = __uint_as_float(__float_as_uint((float)r) | 1u);
                     const float t = __fadd_rn(x, (float)ex.e[l]);
-                    lo = __float_as_uint(t) - ex.eb[l];
+                    lo = __float_as_uint(t);  // raw: digit + bits(E_l)
                     if (l + 1 < K) r = (V)__fsub_rn((float)r, __fsub_rn(t, (float)ex.e[l]));
                 }
                 const uint32_t off = 128u * (uint32_t)(j * GL * CW + l * Cfg::LIMBS);
@@ -183,20 +217,36 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
     bool bad = false;
     const int64_t nq = (row1 - row0) / LEAN_U;  // whole quads (row0 % 4 == 0)
     int it = 0;
-    for (int64_t q0 = 0; q0 < nq; q0 += LEAN_TPB) {  // warp-uniform trip count
-        const int64_t q = q0 + tid;
+    // software pipeline: the next quad's loads are in flight while this one
+    // is deposited
+    int4 kk = make_int4(0, 0, 0, 0);
+    V cv[SRC::NCOL][4];
+    auto load_quad = [&](int64_t q) {
         if (q < nq) {
             const int64_t r = row0 + q * LEAN_U;
-            const int4 kk = __ldcs(reinterpret_cast<const int4 *>(keys + r));
-            V cv[SRC::NCOL][4];
+            kk = __ldcs(reinterpret_cast<const int4 *>(keys + r));
 #pragma unroll
             for (int j = 0; j < SRC::NCOL; ++j) LeanVec<DT>::load(src.col[j] + r, cv[j]);
-            const int32_t ks[4] = {kk.x, kk.y, kk.z, kk.w};
+        }
+    };
+    if (LEAN_PIPE) load_quad(tid);
+    for (int64_t q0 = 0; q0 < nq; q0 += LEAN_TPB) {  // warp-uniform trip count
+        const int64_t q = q0 + tid;
+        if (!LEAN_PIPE) load_quad(q);
+        int4 k_cur = kk;
+        V c_cur[SRC::NCOL][4];
+#pragma unroll
+        for (int j = 0; j < SRC::NCOL; ++j)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c_cur[j][u] = cv[j][u];
+        if (LEAN_PIPE) load_quad(q + LEAN_TPB);
+        if (q < nq) {
+            const int32_t ks[4] = {k_cur.x, k_cur.y, k_cur.z, k_cur.w};
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 V c[SRC::NCOL];
 #pragma unroll
-                for (int j = 0; j < SRC::NCOL; ++j) c[j] = cv[j][u];
+                for (int j = 0; j < SRC::NCOL; ++j) c[j] = c_cur[j][u];
                 take(ks[u], c, bad);
             }
         }
