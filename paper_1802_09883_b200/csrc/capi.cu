@@ -456,7 +456,8 @@ int enqueue_multi(const int32_t *keys, const void *const *cols, int32_t ncols, i
         *flags_out = w.flags;
         if (phase & 1) {
             if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
-            int rc = timed("onchip_accumulate", st, [&] {
+            const char *label = lean_multi_applies(dt, proj, ncols, keys, cols, G) ? "lean_multi" : "onchip_accumulate";
+            int rc = timed(label, st, [&] {
                 return launch_onchip_multi(dt, K, proj, ncols, keys, cols, n, G, w.kglob, w.slots, w.flags, st,
                                            &t_launches);
             });

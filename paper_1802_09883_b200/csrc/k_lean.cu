@@ -364,6 +364,14 @@ int launch_lean_t(const int32_t *keys, const SRC &src, int64_t n, int32_t G, int
 
 }  // namespace
 
+// whether launch_lean_multi takes this call (for the per-kernel timing label)
+bool lean_multi_applies(int DT, int proj, int ncols, const int32_t *keys, const void *const *cols, int32_t G) {
+    if (G > LEAN_GL || lean_disabled() || proj != 1 || DT != 1 || ncols != 4) return false;
+    uintptr_t al = (uintptr_t)keys;
+    for (int j = 0; j < ncols; ++j) al |= (uintptr_t)cols[j];
+    return (al & 15) == 0;
+}
+
 // 0 = launched, 1 = shape not handled here (the caller uses the on-chip
 // kernel), < 0 = error.  Needs 16-byte aligned key and value columns, G <= 4.
 int launch_lean_multi(int DT, int K, int proj, int ncols, const int32_t *keys, const void *const *cols, int64_t n,
