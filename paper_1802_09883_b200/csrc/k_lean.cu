@@ -366,7 +366,10 @@ int launch_lean_t(const int32_t *keys, const SRC &src, int64_t n, int32_t G, int
 
 // whether launch_lean_multi takes this call (for the per-kernel timing label)
 bool lean_multi_applies(int DT, int proj, int ncols, const int32_t *keys, const void *const *cols, int32_t G) {
-    if (G > LEAN_GL || lean_disabled() || proj != 1 || DT != 1 || ncols != 4) return false;
+    if (G > LEAN_GL || lean_disabled()) return false;
+    const bool shape = proj == 1 ? (DT == 1 && ncols == 4) : proj == 2 ? ncols == 1
+                                                                          : (ncols == 1 || ncols == 2 || ncols == 4);
+    if (!shape) return false;
     uintptr_t al = (uintptr_t)keys;
     for (int j = 0; j < ncols; ++j) al |= (uintptr_t)cols[j];
     return (al & 15) == 0;
@@ -377,10 +380,6 @@ bool lean_multi_applies(int DT, int proj, int ncols, const int32_t *keys, const 
 int launch_lean_multi(int DT, int K, int proj, int ncols, const int32_t *keys, const void *const *cols, int64_t n,
                       int32_t G, int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
                       int *launches) {
-    if (G > LEAN_GL || lean_disabled()) return 1;
-    uintptr_t al = (uintptr_t)keys;
-    for (int j = 0; j < ncols; ++j) al |= (uintptr_t)cols[j];
-    if (al & 15) return 1;
 #define LEAN_K(dt, SRCT)                                                                                       \
     do {                                                                                                       \
         SRCT src;                                                                                              \
@@ -394,11 +393,28 @@ int launch_lean_multi(int DT, int K, int proj, int ncols, const int32_t *keys, c
         }                                                                                                      \
         return 1;                                                                                              \
     } while (0)
-    if (proj == 1) {
-        if (DT != 1 || ncols != 4) return 1;
-        LEAN_K(1, SrcQ1);
+    if (!lean_multi_applies(DT, proj, ncols, keys, cols, G)) return 1;
+    using C64_1 = SrcCols<1, 1>;
+    using C64_2 = SrcCols<1, 2>;
+    using C64_4 = SrcCols<1, 4>;
+    using C32_1 = SrcCols<0, 1>;
+    using C32_2 = SrcCols<0, 2>;
+    using C32_4 = SrcCols<0, 4>;
+    using M64 = SrcMoments<1>;
+    using M32 = SrcMoments<0>;
+    if (proj == 1) LEAN_K(1, SrcQ1);
+    if (proj == 2) {
+        if (DT == 1) LEAN_K(1, M64);
+        LEAN_K(0, M32);
     }
-    return 1;
+    if (DT == 1) {
+        if (ncols == 1) LEAN_K(1, C64_1);
+        if (ncols == 2) LEAN_K(1, C64_2);
+        LEAN_K(1, C64_4);
+    }
+    if (ncols == 1) LEAN_K(0, C32_1);
+    if (ncols == 2) LEAN_K(0, C32_2);
+    LEAN_K(0, C32_4);
 #undef LEAN_K
 }
 

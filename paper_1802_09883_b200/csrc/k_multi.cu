@@ -41,7 +41,7 @@ int launch_onchip_multi(int DT, int K, int proj, int ncols, const int32_t *keys,
         }                                                                                                     \
         return -1;                                                                                            \
     } while (0)
-    // config-4 shape with a handful of groups: per-thread register state
+    // a handful of groups (config 4's shape): per-warp lane-copy tables
     // (k_lean.cu); 1 = not handled there
     const int lr = launch_lean_multi(DT, K, proj, ncols, keys, cols, n, G, kglob, slots, status, st, launches);
     if (lr != 1) return lr;

@@ -80,6 +80,44 @@ def test_config4_lean_block_fallback(R, where, what):
     check(R, keys, cols, 4, 3, 1, path=2)
 
 
+@pytest.mark.parametrize("dtype,ncols,G", [(np.float64, 1, 4), (np.float64, 2, 3), (np.float64, 4, 1),
+                                           (np.float32, 1, 2), (np.float32, 2, 4), (np.float32, 4, 4)])
+def test_independent_columns_few_groups(R, variant, dtype, ncols, G):
+    """Few groups: the lean kernel (variant 0) on single-window data, and on
+    data spanning many windows (every block falls back)."""
+    rng = np.random.default_rng(ncols * 100 + G)
+    n = (1 << 20) + 7
+    keys = rng.integers(0, G, n).astype(np.int32)
+    one_window = [(rng.uniform(1, 2, n) * np.where(rng.random(n) < 0.5, -1, 1)).astype(dtype) for _ in range(ncols)]
+    check(R, keys, one_window, G, 3 if dtype == np.float64 else 2, 0, path=2)
+    spread = [(rng.standard_normal(n) * 2.0 ** rng.integers(-20, 20, n)).astype(dtype) for _ in range(ncols)]
+    check(R, keys, spread, G, 3 if dtype == np.float64 else 2, 0, path=2)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_moments_few_groups(R, variant, dtype):
+    rng = np.random.default_rng(5)
+    n = (1 << 20) + 3
+    keys = rng.integers(0, 3, n).astype(np.int32)
+    vals = (rng.uniform(1, 2, n) * 3.0).astype(dtype)
+    got = R.groupby_moments(dev(keys), dev(vals), 3, 3)
+    rc, ref = O.groupby_moments(keys, vals, 3, 3)
+    assert rc == O.OK
+    for k in ("sum", "avg", "var", "stddev", "count"):
+        assert got[k].cpu().numpy().tobytes() == ref[k].tobytes(), k
+
+
+def test_lean_kernel_is_the_one_that_runs(R):
+    keys, cols = synth.generate(4, n=1 << 20)
+    R.timing_enable(True)
+    R.timing_collect()
+    R.groupby_sum_multi(dev(keys), [dev(c) for c in cols], 4, 3, proj=1)
+    torch.cuda.synchronize()
+    names = R.timing_collect()
+    R.timing_enable(False)
+    assert "lean_multi" in names and "onchip_accumulate" not in names
+
+
 def test_config4_lean_errors(R):
     keys, cols = synth.generate(4, n=1 << 20)
     cols = [c.copy() for c in cols]
