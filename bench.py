@@ -331,8 +331,11 @@ def main():
             return
         acc.reset()
         acc.deposit(keys, cols[0])
-        rdist.allreduce_state(acc)
-        acc.finalize(out)
+        if G >= 4096:  # reduce-scatter by group range + all-gather of the results
+            rdist.reduce_scatter_finalize(acc, out)
+        else:
+            rdist.allreduce_state(acc)
+            acc.finalize(out)
 
     for _ in range(max(args.warmup, 3)):
         step()

@@ -33,6 +33,52 @@ def allreduce_state(acc, group=None):
     return acc
 
 
+def reduce_scatter_finalize(acc, out, group=None):
+    """SURVEY.md 8(e) with a reduce-scatter by contiguous group range (less
+    traffic than allreduce_state at high group counts):
+
+      1. all-reduce MAX on the window tops;
+      2. realign to the global tops (window_export);
+      3. reduce-scatter SUM of the limbs: rank r receives groups
+         [r * P, (r + 1) * P), P = ceil(G / world);
+      4. canonicalise and finalise the owned range (window_import range form);
+      5. all-gather the finalised values into `out` (every rank, all groups).
+
+    Integer SUM / MAX only, so `out` is bit-identical for any rank count.
+    Afterwards each rank's handle holds the combined state of ITS range only.
+    Backends without reduce-scatter (gloo) take the all-reduce + slice form of
+    step 3 (same integers)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    G, K = acc.n_groups, acc.fold
+    k = acc.top_levels()
+    dist.all_reduce(k, op=dist.ReduceOp.MAX, group=group)
+    limbs = acc.window_export(k)
+    per = -(-G // world)
+    width = 2 * K
+    padded = torch.zeros(per * world * width, dtype=torch.int64, device=limbs.device)
+    padded[: G * width].copy_(limbs)
+    if dist.get_backend(group) == "nccl":
+        mine = torch.empty(per * width, dtype=torch.int64, device=limbs.device)
+        dist.reduce_scatter_tensor(mine, padded, op=dist.ReduceOp.SUM, group=group)
+    else:
+        dist.all_reduce(padded, op=dist.ReduceOp.SUM, group=group)
+        mine = padded[rank * per * width:(rank + 1) * per * width].clone()
+    g0 = rank * per
+    cnt = max(0, min(per, G - g0))
+    if cnt:
+        acc.window_import(k[g0:g0 + cnt].contiguous(), mine[: cnt * width].contiguous(), g0=g0, count=cnt)
+    local = torch.as_tensor(acc.finalize())
+    part = torch.zeros(per, dtype=local.dtype, device=local.device)
+    if cnt:
+        part[:cnt] = local[g0:g0 + cnt]
+    parts = [torch.empty_like(part) for _ in range(world)]
+    dist.all_gather(parts, part, group=group)
+    full = torch.cat(parts)[:G]
+    out.copy_(full.to(out.device))
+    return out
+
+
 def allreduce_table(flags, kglob, slots, group=None):
     """Combine the per-rank absolute-level slot tables of the fused
     multi-column pass (repro_groupby_multi_table views): status bits OR-ed

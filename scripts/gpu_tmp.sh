@@ -1,2 +1,2 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gpu_multi.py -q -x 2>&1 | tail -5
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "exchange" 2>&1 | tail -3

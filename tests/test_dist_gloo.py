@@ -28,6 +28,7 @@ class OracleAccumulator:
 
     def __init__(self, keys, vals, G, K):
         self.G, self.K = G, K
+        self.n_groups, self.fold = G, K
         self.dtype = O.F64 if vals.dtype == np.float64 else O.F32
         rc, _, st = O.groupby_sum(keys, vals, G, K, threads=1, with_state=True)
         assert rc == O.OK
@@ -59,10 +60,13 @@ class OracleAccumulator:
                 out[g, l, 1] = T[l] >> 32
         return torch.from_numpy(out.reshape(-1))
 
-    def window_import(self, k_global, limbs):
-        L = limbs.numpy().reshape(self.G, self.K, 2)
-        self.k = k_global.numpy().astype(np.int64)
-        self.T = [[(int(L[g, l, 1]) << 32) + int(L[g, l, 0]) for l in range(self.K)] for g in range(self.G)]
+    def window_import(self, k_global, limbs, g0=0, count=None):
+        count = self.G - g0 if count is None else count
+        L = limbs.numpy().reshape(count, self.K, 2)
+        kg = k_global.numpy().astype(np.int64)
+        for i in range(count):
+            self.k[g0 + i] = kg[i]
+            self.T[g0 + i] = [(int(L[i, l, 1]) << 32) + int(L[i, l, 0]) for l in range(self.K)]
         return self
 
     def finalize(self):
@@ -79,7 +83,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, keys, vals, G, K, shard, q):
+def _worker(rank, world, port, keys, vals, G, K, shard, q, exchange="allreduce"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -91,17 +95,25 @@ def _worker(rank, world, port, keys, vals, G, K, shard, q):
         else:
             k, v = keys[rank::world], vals[rank::world]
         acc = OracleAccumulator(k, v, G, K)
-        rdist.allreduce_state(acc)
-        q.put((rank, acc.finalize().tobytes()))
+        if exchange == "reduce_scatter":
+            out = torch.empty(G, dtype=torch.float64 if vals.dtype == np.float64 else torch.float32)
+            rdist.reduce_scatter_finalize(acc, out)
+            q.put((rank, out.numpy().tobytes()))
+        else:
+            rdist.allreduce_state(acc)
+            q.put((rank, acc.finalize().tobytes()))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("dtype,K,shard", [(np.float64, 3, "contiguous"), (np.float64, 2, "strided"),
-                                           (np.float32, 2, "contiguous")])
-def test_two_rank_exchange_equals_single_oracle(dtype, K, shard):
+@pytest.mark.parametrize("dtype,K,shard,exchange,world,G", [
+    (np.float64, 3, "contiguous", "allreduce", 2, 12), (np.float64, 2, "strided", "allreduce", 2, 12),
+    (np.float32, 2, "contiguous", "allreduce", 2, 12),
+    (np.float64, 3, "contiguous", "reduce_scatter", 2, 13), (np.float32, 2, "strided", "reduce_scatter", 3, 7),
+    (np.float64, 2, "contiguous", "reduce_scatter", 3, 2)])
+def test_two_rank_exchange_equals_single_oracle(dtype, K, shard, exchange, world, G):
     rng = np.random.default_rng(11)
-    n, G = 6000, 12
+    n = 6000
     keys = rng.integers(0, G, n, dtype=np.int32)
     e = rng.integers(-30, 31, n)
     vals = (rng.uniform(1, 2, n) * np.exp2(e) * rng.choice([-1, 1], n)).astype(dtype)
@@ -111,14 +123,15 @@ def test_two_rank_exchange_equals_single_oracle(dtype, K, shard):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, keys, vals, G, K, shard, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, keys, vals, G, K, shard, q, exchange))
+             for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=120) for _ in range(2))
+    res = dict(q.get(timeout=120) for _ in range(world))
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert res[0] == res[1] == ref.tobytes()
+    assert all(res[r] == ref.tobytes() for r in range(world))
 
 
 def test_shard_rows_cover_everything():

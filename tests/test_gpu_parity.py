@@ -297,6 +297,35 @@ def test_window_exchange_emulates_ranks(R):
     assert_bits_equal(accs[1].finalize().cpu().numpy(), ref)
 
 
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_reduce_scatter_exchange_emulates_ranks(R, world):
+    """dist.reduce_scatter_finalize's steps on one GPU: each emulated rank
+    imports only its contiguous group range (window_import range form) and
+    finalises it; the concatenated ranges equal the oracle."""
+    G = 1000  # not a multiple of world
+    keys, vals = synth.generate_chunked(1, 1 << 19, G)
+    vals = vals.copy()
+    vals[:1000] *= 2.0 ** 70
+    ref = oracle_groupby(keys, vals, G, 3)
+    accs = []
+    for r in range(world):
+        a = R.Accumulator(G, 3, R.F64)
+        a.deposit(dev(keys[r::world]), dev(vals[r::world]))
+        accs.append(a)
+    kg = accs[0].top_levels()
+    for a in accs[1:]:
+        kg = torch.maximum(kg, a.top_levels())
+    limbs = sum(a.window_export(kg) for a in accs)
+    per = -(-G // world)
+    parts = []
+    for r, a in enumerate(accs):
+        g0, cnt = r * per, max(0, min(per, G - r * per))
+        if cnt:
+            a.window_import(kg[g0:g0 + cnt].contiguous(), limbs[g0 * 6:(g0 + cnt) * 6].contiguous(), g0=g0, count=cnt)
+            parts.append(a.finalize()[g0:g0 + cnt])
+    assert_bits_equal(torch.cat(parts).cpu().numpy(), ref)
+
+
 def test_host_entry_point_matches(R):
     keys, vals = synth.generate_chunked(1, (1 << 23) + 12345, 1024)
     kt, vt = torch.from_numpy(keys).pin_memory(), torch.from_numpy(vals).pin_memory()
