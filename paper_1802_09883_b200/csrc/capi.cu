@@ -268,7 +268,7 @@ int enqueue_groupby(const int32_t *keys, const void *vals, int64_t n, int32_t G,
         OnchipWs w = carve_onchip(ws, n, G, K, dt);
         *flags_out = w.flags;
         if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
-        int rc = timed("onchip_accumulate", st, [&] {
+        int rc = timed(lean_single_applies(keys, vals, G) ? "lean_single" : "onchip_accumulate", st, [&] {
             return launch_onchip_any(dt, K, keys, vals, n, G, w.kglob, w.slots, w.flags, st, &t_launches);
         });
         if (rc) return map_launch(rc);

@@ -43,6 +43,9 @@ int launch_rsum(int DT, int K, const void *x, const void *y, int64_t n, int32_t 
                 uint32_t *status, cudaStream_t st, int *launches);
 int launch_onchip_array(int DT, int K, const void *x, const void *y, int64_t n, int32_t *kglob,
                         unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches);
+bool lean_single_applies(const int32_t *keys, const void *vals, int32_t G);
+int launch_lean_single(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G, int32_t *kglob,
+                       unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches);
 bool lean_multi_applies(int DT, int proj, int ncols, const int32_t *keys, const void *const *cols, int32_t G);
 int launch_lean_multi(int DT, int K, int proj, int ncols, const int32_t *keys, const void *const *cols, int64_t n,
                       int32_t G, int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,

@@ -45,11 +45,11 @@ bool lean_disabled() { return onchip_variant() != 0; }  // variants 1-3 force th
 #define LEAN_MINB 1  // resident blocks per SM the register budget is sized for
 #endif
 constexpr int LEAN_TPB = 256;  // = OnchipCfg::TPB (the fallback runs accumulate_range)
-constexpr int LEAN_GL = 4;     // groups handled
+constexpr int LEAN_GL = 4;     // groups handled (multi-column sources)
+constexpr int LEAN_GL1 = 16;   // groups handled (single column)
 constexpr int LEAN_U = 4;      // rows per thread per iteration
 // a lane copy takes <= 1 limb per row of its lane; the 32 copies of a counter
 // are summed in 32 bits, so a fold is due every 4095 / 32 rows per lane
-constexpr int LEAN_FOLD_IT = 4095 / 32 / LEAN_U;  // iterations between folds (31)
 
 template <int DT>
 struct LeanVec;
@@ -69,29 +69,31 @@ struct LeanVec<0> {  // 4 floats = one 16-byte load
     }
 };
 
-template <int DT, int K, class SRC>
+template <int DT, int K, class SRC, int GL>
 struct LeanGeom {
     static constexpr int NV = SRC::NV;
     static constexpr int ND = SRC::ONES ? NV - 1 : NV;  // virtual columns with digits
     static constexpr int CW = K * Fmt<DT>::LIMBS;        // counter words per virtual group
-    static constexpr int NPOS = ND * LEAN_GL * CW;       // counter positions per warp (x 32 lanes)
-    static constexpr int WORDS = (NPOS + LEAN_GL) * 32;  // + COUNT copies
-    static constexpr size_t WARP_BYTES = 4 * (size_t)WORDS + 8 * (size_t)(NPOS + LEAN_GL);  // + int64 sums
+    static constexpr int NPOS = ND * GL * CW;            // counter positions per warp (x 32 lanes)
+    static constexpr int WORDS = (NPOS + GL) * 32;       // + per-group row counts
+    static constexpr size_t WARP_BYTES = 4 * (size_t)WORDS + 8 * (size_t)(NPOS + GL);  // + int64 sums
     static constexpr size_t BYTES = WARP_BYTES * (LEAN_TPB / 32);
+    static_assert(ND * GL <= 32, "one bit per (column, group) in the window masks");
 };
 
-template <int DT, int K, class SRC>
+template <int DT, int K, class SRC, int GL>
 __global__ void __launch_bounds__(LEAN_TPB, LEAN_MINB)
 k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t G, int64_t chunk,
              int32_t *__restrict__ kglob, unsigned long long *__restrict__ slots, uint32_t *__restrict__ status) {
     using F = Fmt<DT>;
     using V = typename F::V;
-    using Geo = LeanGeom<DT, K, SRC>;
+    using Geo = LeanGeom<DT, K, SRC, GL>;
     using Cfg = OnchipCfg<DT, K>;
-    constexpr int NV = Geo::NV, ND = Geo::ND, CW = Geo::CW, NPOS = Geo::NPOS, GL = LEAN_GL;
+    constexpr int NV = Geo::NV, ND = Geo::ND, CW = Geo::CW, NPOS = Geo::NPOS;
     constexpr int NS = F::KMAX + K;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_bad, s_k0;
+    __shared__ uint32_t s_present, s_seen;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t row0 = (int64_t)blockIdx.x * chunk;
@@ -104,22 +106,36 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
     int64_t *wsum = reinterpret_cast<int64_t *>(wt + Geo::WORDS);
     for (int i = lane; i < Geo::WORDS; i += 32) wt[i] = 0;
     for (int i = lane; i < NPOS + GL; i += 32) wsum[i] = 0;
-    if (tid == 0) {  // the block's window k0: k* of the first row's first digit column
+    if (tid == 0) {
         s_bad = 0;
-        V c[SRC::NCOL];
+        s_k0 = 0;
+        s_present = 0;
+        s_seen = 0;
+    }
+    __syncthreads();
+    {  // the block's window k0: the largest k* among the first LEAN_TPB rows
+        const int64_t r = row0 + tid;
+        if (r < row1) {
+            V c[SRC::NCOL];
 #pragma unroll
-        for (int j = 0; j < SRC::NCOL; ++j) c[j] = src.col[j][row0];
-        int32_t vk[NV];
-        V vv[NV];
-        src.expand(0, c, vk, vv);
-        uint32_t f = 0;
-        const int k = kstar_of<DT>(vv[0], f);
-        s_k0 = k < 0 ? 0 : k;
+            for (int j = 0; j < SRC::NCOL; ++j) c[j] = src.col[j][r];
+            int32_t vk[NV];
+            V vv[NV];
+            src.expand(0, c, vk, vv);
+            int km = 0;
+#pragma unroll
+            for (int j = 0; j < ND; ++j) {
+                uint32_t f = 0;
+                km = max(km, kstar_of<DT>(vv[j], f));
+            }
+            km = __reduce_max_sync(__activemask(), km);  // active lanes are a prefix: lane 0 is one
+            if (lane == 0) atomicMax(&s_k0, km);
+        }
     }
     __syncthreads();
     const int k0 = s_k0;
-    // k*(b) == k0  <=>  lo <= |b| < hi on the magnitude bits; k0 == 0 admits
-    // everything below hi (zero and denormals included)
+    // k*(b) <= k0  <=>  |b| < hi on the magnitude bits (NaN/Inf fail it);
+    // k*(b) == k0  <=>  also |b| >= lo (k0 > 0), tracked per (column, group)
     const uint32_t sh = DT == 1 ? 20 : 23;
     const uint32_t hi_b = (uint32_t)(F::W * k0 + F::W - 1 - F::m + F::BIAS) << sh;
     const uint32_t lo_b = k0 == 0 ? 0u : (uint32_t)(F::W * (k0 - 1) + F::W - 1 - F::m + F::BIAS) << sh;
@@ -131,7 +147,7 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
     // sums and clear them.  The counters hold RAW limbs (see take): the sum
     // of a position is corrected by (rows of its group since the last fold) x
     // (the limb's constant bias), mod 2^32 -- exact, since the true sum of at
-    // most 32 x 4 x LEAN_FOLD_IT balanced limbs fits an int32.
+    // most 32 x 4Q x FOLD_IT <= 4095 balanced limbs fits an int32.
     auto copies_sum = [&](int p) {
         uint4 *c = reinterpret_cast<uint4 *>(wt + (size_t)p * 32);
         uint32_t s = 0;
@@ -151,11 +167,11 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
             ng = copies_sum(NPOS + lane);
             wsum[NPOS + lane] += (int64_t)ng;
         }
-        uint32_t N[GL];
-#pragma unroll
-        for (int g = 0; g < GL; ++g) N[g] = __shfl_sync(0xffffffffu, ng, g);
-        for (int p = lane; p < NPOS; p += 32) {
+        for (int p0 = 0; p0 < NPOS; p0 += 32) {  // warp-uniform trip count (shuffles below)
+            const int p = p0 + lane;
             const int g = (p / CW) % GL, w = p % CW;
+            const uint32_t nsel = __shfl_sync(0xffffffffu, ng, g);  // rows of group g since the last fold
+            if (p >= NPOS) continue;
             uint32_t bias;
             if (DT == 1) {
                 bias = (w & 1) ? 0x80000000u : 0x80000u;  // hi: exponent field of E_l; lo: the 2^19 offset
@@ -163,9 +179,6 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
                 const int ue = F::W * (k0 - w) - F::m;  // binary32: one limb per level, bias = bits(E_l)
                 bias = ((uint32_t)(ue + F::m + F::BIAS) << 23) | (1u << 22);
             }
-            uint32_t nsel = N[0];
-#pragma unroll
-            for (int q = 1; q < GL; ++q) nsel = g == q ? N[q] : nsel;
             const uint32_t s = copies_sum(p) - bias * nsel;
             wsum[p] += (int64_t)(int32_t)s;
         }
@@ -177,6 +190,7 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
     // removed at the fold), one conflict-free atomic per limb, +1 on the
     // group's COUNT copy.
     // Position (j * GL + g) * CW + w sits at byte 128 * position of the table.
+    uint32_t present = 0, seen = 0;  // groups with rows; (column, group) with a value at k0
     auto take = [&](int32_t key, const V (&c)[SRC::NCOL], bool &bad) {
         int32_t vk[NV];
         V vv[NV];
@@ -184,11 +198,14 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
         bad |= (uint32_t)key >= (uint32_t)G;
         const uint32_t g = (uint32_t)key & (GL - 1);
         const uint32_t kb = tbase + 128u * CW * g;
+        const uint32_t gbit = 1u << g;
+        present |= gbit;
 #pragma unroll
         for (int j = 0; j < ND; ++j) {
             const uint32_t a = (DT == 1 ? (uint32_t)__double2hiint((double)vv[j]) : __float_as_uint((float)vv[j])) &
                                0x7FFFFFFFu;
-            bad |= (a - lo_b) >= (hi_b - lo_b);
+            bad |= a >= hi_b;
+            seen |= a >= lo_b ? gbit << (j * GL) : 0u;
             V r = vv[j];
 #pragma unroll
             for (int l = 0; l < K; ++l) {
@@ -216,38 +233,53 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
 
     bool bad = false;
     const int64_t nq = (row1 - row0) / LEAN_U;  // whole quads (row0 % 4 == 0)
+    // Q quads per thread per step (interleaved: quad q0 + i * TPB + tid, so
+    // every 16-byte load instruction of a warp is contiguous); Q grows as the
+    // row gets narrower, keeping ~128-192 bytes per lane in flight
+    constexpr int Q = SRC::NCOL == 1 ? 4 : SRC::NCOL == 2 ? 2 : 1;
+    constexpr int FOLD_IT = 4095 / 32 / (LEAN_U * Q);  // a lane copy takes <= 4Q rows per step
     int it = 0;
-    // software pipeline: the next quad's loads are in flight while this one
+    // software pipeline: the next step's loads are in flight while this one
     // is deposited
-    int4 kk = make_int4(0, 0, 0, 0);
-    V cv[SRC::NCOL][4];
-    auto load_quad = [&](int64_t q) {
-        if (q < nq) {
-            const int64_t r = row0 + q * LEAN_U;
-            kk = __ldcs(reinterpret_cast<const int4 *>(keys + r));
+    int4 kk[Q];
+    V cv[Q][SRC::NCOL][4];
+    auto load_step = [&](int64_t q0) {
 #pragma unroll
-            for (int j = 0; j < SRC::NCOL; ++j) LeanVec<DT>::load(src.col[j] + r, cv[j]);
+        for (int i = 0; i < Q; ++i) {
+            const int64_t q = q0 + i * LEAN_TPB + tid;
+            if (q < nq) {
+                const int64_t r = row0 + q * LEAN_U;
+                kk[i] = __ldcs(reinterpret_cast<const int4 *>(keys + r));
+#pragma unroll
+                for (int j = 0; j < SRC::NCOL; ++j) LeanVec<DT>::load(src.col[j] + r, cv[i][j]);
+            }
         }
     };
-    if (LEAN_PIPE) load_quad(tid);
-    for (int64_t q0 = 0; q0 < nq; q0 += LEAN_TPB) {  // warp-uniform trip count
-        const int64_t q = q0 + tid;
-        if (!LEAN_PIPE) load_quad(q);
-        int4 k_cur = kk;
-        V c_cur[SRC::NCOL][4];
+    if (LEAN_PIPE) load_step(0);
+    for (int64_t q0 = 0; q0 < nq; q0 += Q * LEAN_TPB) {  // warp-uniform trip count
+        if (!LEAN_PIPE) load_step(q0);
+        int4 k_cur[Q];
+        V c_cur[Q][SRC::NCOL][4];
 #pragma unroll
-        for (int j = 0; j < SRC::NCOL; ++j)
+        for (int i = 0; i < Q; ++i) {
+            k_cur[i] = kk[i];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) c_cur[j][u] = cv[j][u];
-        if (LEAN_PIPE) load_quad(q + LEAN_TPB);
-        if (q < nq) {
-            const int32_t ks[4] = {k_cur.x, k_cur.y, k_cur.z, k_cur.w};
+            for (int j = 0; j < SRC::NCOL; ++j)
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                V c[SRC::NCOL];
+                for (int u = 0; u < 4; ++u) c_cur[i][j][u] = cv[i][j][u];
+        }
+        if (LEAN_PIPE) load_step(q0 + Q * LEAN_TPB);
 #pragma unroll
-                for (int j = 0; j < SRC::NCOL; ++j) c[j] = c_cur[j][u];
-                take(ks[u], c, bad);
+        for (int i = 0; i < Q; ++i) {
+            if (q0 + i * LEAN_TPB + tid < nq) {
+                const int32_t ks[4] = {k_cur[i].x, k_cur[i].y, k_cur[i].z, k_cur[i].w};
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    V c[SRC::NCOL];
+#pragma unroll
+                    for (int j = 0; j < SRC::NCOL; ++j) c[j] = c_cur[i][j][u];
+                    take(ks[u], c, bad);
+                }
             }
         }
         // a value outside the lean path anywhere in the block: stop (the
@@ -257,7 +289,7 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
             bad = true;
             break;
         }
-        if (++it == LEAN_FOLD_IT) {
+        if (++it == FOLD_IT) {
             fold();
             it = 0;
         }
@@ -272,6 +304,21 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
             take(keys[r], c, bad);
         }
         if (bad) atomicOr(&s_bad, 1);
+    }
+    present = __reduce_or_sync(0xffffffffu, present);
+    seen = __reduce_or_sync(0xffffffffu, seen);
+    if (lane == 0) {
+        atomicOr(&s_present, present);
+        atomicOr(&s_seen, seen);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // every (column, group) the block touched needs a value AT k0, or its
+        // top in this block is lower and the levels under k0 - K + 1 that were
+        // dropped may be needed: such a block takes the generic code
+#pragma unroll
+        for (int j = 0; j < ND; ++j)
+            if (s_present & ~(s_seen >> (j * GL)) & (GL == 32 ? 0xffffffffu : (1u << GL) - 1u)) s_bad = 1;
     }
     __syncthreads();
 
@@ -327,17 +374,17 @@ k_lean_multi(const int32_t *__restrict__ keys, const SRC src, int64_t n, int32_t
     }
 }
 
-template <int DT, int K, class SRC>
+template <int DT, int K, class SRC, int GL>
 int launch_lean_t(const int32_t *keys, const SRC &src, int64_t n, int32_t G, int32_t *kglob,
                   unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches) {
-    using Geo = LeanGeom<DT, K, SRC>;
-    if (G > LEAN_GL) return 1;
+    using Geo = LeanGeom<DT, K, SRC, GL>;
+    if (G > GL) return 1;
     const int32_t Gv = G * SRC::NV;
     // the lean tables, or the fallback's shared table (register level sums,
     // register loads) -- whichever is larger (the two are never live together)
     const size_t fb = (onchip_table_bytes<DT, K>(Gv, true) + 127) & ~(size_t)127;
     const size_t smem = std::max(fb, Geo::BYTES);
-    auto kern = k_lean_multi<DT, K, SRC>;
+    auto kern = k_lean_multi<DT, K, SRC, GL>;
     if (smem > (size_t)device_props().smem_optin) return 1;
     static thread_local size_t configured = 0;
     if (configured < smem) {
@@ -386,10 +433,10 @@ int launch_lean_multi(int DT, int K, int proj, int ncols, const int32_t *keys, c
         for (int j = 0; j < SRCT::NCOL; ++j) src.col[j] = (const typename Fmt<dt>::V *)cols[j];               \
         src.G = G;                                                                                             \
         switch (K) {                                                                                           \
-            case 1: return launch_lean_t<dt, 1, SRCT>(keys, src, n, G, kglob, slots, status, st, launches);    \
-            case 2: return launch_lean_t<dt, 2, SRCT>(keys, src, n, G, kglob, slots, status, st, launches);    \
-            case 3: return launch_lean_t<dt, 3, SRCT>(keys, src, n, G, kglob, slots, status, st, launches);    \
-            case 4: return launch_lean_t<dt, 4, SRCT>(keys, src, n, G, kglob, slots, status, st, launches);    \
+            case 1: return launch_lean_t<dt, 1, SRCT, LEAN_GL>(keys, src, n, G, kglob, slots, status, st, launches); \
+            case 2: return launch_lean_t<dt, 2, SRCT, LEAN_GL>(keys, src, n, G, kglob, slots, status, st, launches); \
+            case 3: return launch_lean_t<dt, 3, SRCT, LEAN_GL>(keys, src, n, G, kglob, slots, status, st, launches); \
+            case 4: return launch_lean_t<dt, 4, SRCT, LEAN_GL>(keys, src, n, G, kglob, slots, status, st, launches); \
         }                                                                                                      \
         return 1;                                                                                              \
     } while (0)
@@ -416,6 +463,33 @@ int launch_lean_multi(int DT, int K, int proj, int ncols, const int32_t *keys, c
     if (ncols == 2) LEAN_K(0, C32_2);
     LEAN_K(0, C32_4);
 #undef LEAN_K
+}
+
+// Single-column GroupBy with at most LEAN_GL1 groups (16-byte aligned
+// columns): 0 = launched, 1 = not handled here.
+bool lean_single_applies(const int32_t *keys, const void *vals, int32_t G) {
+    return G <= LEAN_GL1 && !lean_disabled() && (((uintptr_t)keys | (uintptr_t)vals) & 15) == 0;
+}
+
+int launch_lean_single(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G, int32_t *kglob,
+                       unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches) {
+    if (!lean_single_applies(keys, vals, G)) return 1;
+#define LEAN_S(dt)                                                                                               \
+    do {                                                                                                         \
+        SrcSingle<dt> src;                                                                                       \
+        src.col[0] = (const typename Fmt<dt>::V *)vals;                                                          \
+        src.G = G;                                                                                               \
+        switch (K) {                                                                                             \
+            case 1: return launch_lean_t<dt, 1, SrcSingle<dt>, LEAN_GL1>(keys, src, n, G, kglob, slots, status, st, launches); \
+            case 2: return launch_lean_t<dt, 2, SrcSingle<dt>, LEAN_GL1>(keys, src, n, G, kglob, slots, status, st, launches); \
+            case 3: return launch_lean_t<dt, 3, SrcSingle<dt>, LEAN_GL1>(keys, src, n, G, kglob, slots, status, st, launches); \
+            case 4: return launch_lean_t<dt, 4, SrcSingle<dt>, LEAN_GL1>(keys, src, n, G, kglob, slots, status, st, launches); \
+        }                                                                                                        \
+        return 1;                                                                                                \
+    } while (0)
+    if (DT == 1) LEAN_S(1);
+    LEAN_S(0);
+#undef LEAN_S
 }
 
 }  // namespace repro

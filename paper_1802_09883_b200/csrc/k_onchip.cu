@@ -77,6 +77,9 @@ int launch_onchip_any(int DT, int K, const int32_t *keys, const void *vals, int6
     // auto (0): the per-row atomic kernel wherever it fits (measured faster at
     // every group count on B200); the tile-sorted kernel only when asked for
     // or when G exceeds the atomic kernel's capacity.
+    // a handful of groups: per-warp lane-copy tables (k_lean.cu); 1 = not taken
+    const int lr = launch_lean_single(DT, K, keys, vals, n, G, kglob, slots, status, st, launches);
+    if (lr != 1) return lr;
     const int v = onchip_variant();
     const bool sorted = (v == 2 && G <= sorted_max_groups(K, DT)) || G > atomic_max_groups(K, DT);
     if (sorted) return launch_sorted_any(DT, K, keys, vals, n, G, kglob, slots, status, st, launches);

@@ -27,9 +27,10 @@ def R():
     return R
 
 
-@pytest.fixture(params=[1, 2, 3], ids=["atomic", "sorted", "regload"])
+@pytest.fixture(params=[0, 1, 2, 3], ids=["auto", "atomic", "sorted", "regload"])
 def variant(R, request):
-    """Run a test under each on-chip kernel (TMA-fed per-row atomics /
+    """Run a test under each on-chip kernel (auto: the lean per-warp kernel for
+    <= 16 groups, else the TMA-fed per-row atomics / TMA-fed per-row atomics /
     tile-sorted runs / per-row atomics with register loads)."""
     R.set_kernel_variant(request.param)
     yield request.param
@@ -324,6 +325,39 @@ def test_reduce_scatter_exchange_emulates_ranks(R, world):
             a.window_import(kg[g0:g0 + cnt].contiguous(), limbs[g0 * 6:(g0 + cnt) * 6].contiguous(), g0=g0, count=cnt)
             parts.append(a.finalize()[g0:g0 + cnt])
     assert_bits_equal(torch.cat(parts).cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("dtype,K,G", [(np.float64, 3, 16), (np.float64, 2, 3), (np.float32, 2, 16),
+                                       (np.float32, 3, 1)])
+@pytest.mark.parametrize("case", ["tiny_group", "late_large", "zeros", "one_window"])
+def test_lean_single_window_checks(R, dtype, K, G, case):
+    """The lean kernel (<= 16 groups) keeps a block only if every value is at
+    or below the block's window k0 and every group it touched has a value AT
+    k0; the cases below force each kind of fallback (and one that needs none).
+    Bits must equal the oracle's either way."""
+    rng = np.random.default_rng(G * 10 + K)
+    n = (1 << 20) + 9
+    keys = rng.integers(0, G, n).astype(np.int32)
+    vals = (rng.uniform(1, 2, n) * np.where(rng.random(n) < 0.5, -1, 1)).astype(dtype)
+    if case == "tiny_group":  # group G-1 holds only values far below the others' window
+        vals[keys == G - 1] *= 2.0 ** -60 if dtype == np.float64 else 2.0 ** -30
+    elif case == "late_large":  # a value above the window late in every block
+        vals[n - 3] = 2.0 ** 100 if dtype == np.float64 else 2.0 ** 40
+        vals[n // 2] = -(2.0 ** 90) if dtype == np.float64 else -(2.0 ** 35)
+    elif case == "zeros":
+        vals[::7] = 0.0
+    got = gpu_groupby(R, keys, vals, G, K)
+    assert_bits_equal(got, oracle_groupby(keys, vals, G, K))
+
+
+def test_lean_single_is_the_one_that_runs(R):
+    keys, vals = synth.generate_chunked(1, 1 << 20, 16)
+    R.timing_enable(True)
+    R.timing_collect()
+    gpu_groupby(R, keys, vals, 16, 3)
+    names = R.timing_collect()
+    R.timing_enable(False)
+    assert "lean_single" in names and "onchip_accumulate" not in names
 
 
 def test_host_entry_point_matches(R):
