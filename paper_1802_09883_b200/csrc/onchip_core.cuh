@@ -468,8 +468,11 @@ struct SrcArray {
 
 // The rows of ONE partition (key >> 10 == part) read in place from the
 // original columns, as local keys 0..1023 of that partition; every other row
-// becomes (key 0, value 0), which deposits nothing and keeps the fast path
-// (the partitioned path's heavy-partition offload, k_partition.cu).
+// becomes (its key's low bits, value 0), which deposits nothing and keeps the
+// fast path (the partitioned path's heavy-partition offload, k_partition.cu).
+// The zero deposits are spread over the groups by the row's own key: sent to
+// one group they would pile up on one shared word (14 bank wavefronts per
+// warp atomic measured for config 3, vs 3.8 for random groups).
 template <int DT>
 struct SrcFiltered {
     using V = typename Fmt<DT>::V;
@@ -482,7 +485,7 @@ struct SrcFiltered {
     int part;  // partition id
     __device__ __forceinline__ void expand(int32_t key, const V (&c)[NCOL], int32_t (&vk)[NV], V (&vv)[NV]) const {
         const bool in = key >= 0 && (key >> 10) == part;
-        vk[0] = in ? (key & 1023) : 0;
+        vk[0] = in || G == 1024 ? (key & 1023) : (key & 1023) % G;
         vv[0] = in ? c[0] : V(0);
     }
 };
