@@ -385,9 +385,12 @@ int32_t repro_onchip_max_groups(int32_t fold, int32_t dtype);
  * Never changes result bits. */
 void repro_set_path_override(int32_t path);
 
-/* Choose the on-chip accumulate kernel for testing: 0 auto (default), 1 the
- * per-row shared-atomic kernel, 2 the tile-sorted kernel.  Never changes
- * result bits. */
+/* Choose the on-chip accumulate kernel for testing: 0 auto (default: the
+ * lean per-warp kernel for <= 16 groups single-column / <= 4 groups
+ * multi-column, the keyless register kernel for repro_sum / repro_dot, else
+ * the TMA-fed per-row shared-atomic kernel), 1 the per-row shared-atomic
+ * kernel, 2 the tile-sorted kernel, 3 the per-row shared-atomic kernel with
+ * register loads (no TMA).  Never changes result bits. */
 void repro_set_kernel_variant(int32_t variant);
 
 /* Per-kernel device timing (benchmark aid).  While enabled, every kernel the
