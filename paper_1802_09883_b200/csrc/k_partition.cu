@@ -47,6 +47,12 @@ constexpr int SEG_NW = SEG_TPB / 32;
 #define SEG_RT_DEF 16
 #endif
 constexpr int SEG_RT = SEG_RT_DEF;           // rows per thread per scatter tile
+#ifndef PART_IPS
+#define PART_IPS 8                           // accumulate work items per SM
+#endif
+#ifndef SEG_HIST_BPS
+#define SEG_HIST_BPS 4                       // histogram blocks per SM (2 -> 4: 0.50 -> 0.35 ms, config 3)
+#endif
 #ifndef SEG_RTH
 #define SEG_RTH 32                           // keys per thread in flight in the histogram
 #endif
@@ -89,6 +95,7 @@ struct Plan {
     int64_t max_items;
     int grid;        // persistent blocks of the hist / scatter kernels
     int hb;          // work items of a heavy partition summed in place
+    int hgrid;       // histogram blocks
 };
 
 // Partitioning depth (f3 of SURVEY.md 8(f)): partition
@@ -127,8 +134,9 @@ Plan make_plan(int64_t n, int32_t G, int DT, int passes = 0) {
     pl.cu = std::max<int64_t>(1 << 14, (n + 8 * sms - 1) / (8 * sms));
     pl.max_units = (n + pl.cu - 1) / pl.cu + (1 << pl.bits[0]) + 1;
     pl.grid = (int)std::max<int64_t>(1, std::min<int64_t>(2 * sms, pl.max_units));
-    // work items: ~8 per SM over the whole input, at least PART_CH rows
-    pl.ch = std::max<int64_t>(PART_CH, (n + 8 * sms - 1) / (8 * sms));
+    pl.hgrid = (int)std::max<int64_t>(1, std::min<int64_t>(SEG_HIST_BPS * sms, pl.max_units));
+    // work items: ~PART_IPS per SM over the whole input, at least PART_CH rows
+    pl.ch = std::max<int64_t>(PART_CH, (n + PART_IPS * sms - 1) / (PART_IPS * sms));
     pl.hb = 2 * sms;
     pl.max_items = (n + pl.ch - 1) / pl.ch + pl.Pf + pl.hb;
     return pl;
@@ -796,7 +804,7 @@ int run_partitioned(const int32_t *keys, const void *vals, int64_t n, int32_t G,
             int tk = trace_begin(st);
             k_seg_units<<<1, 1024, 0, st>>>(pass == 0 ? nullptr : w.base, S, n, pl.cu, w.units, w.useg, w.ufirst);
             ++*launches;
-            k_seg_hist<<<pl.grid, SEG_TPB, 0, st>>>(ik, w.units, w.ufirst, S, pl.shift[pass], bits, G, pass == 0,
+            k_seg_hist<<<pl.hgrid, SEG_TPB, 0, st>>>(ik, w.units, w.ufirst, S, pl.shift[pass], bits, G, pass == 0,
                                                      w.hist, status);
             ++*launches;
             k_seg_scan<<<S * F, 256, 0, st>>>(w.hist, w.ufirst, bits, w.ptot);
