@@ -60,7 +60,7 @@ constexpr int SEG_RT = SEG_RT_DEF;           // rows per thread per scatter tile
 #define PART_HEAVY 1                         // sum a partition with >= n/2 of the rows in place
 #endif
 #ifndef SEG_ONEPASS_BITS64
-#define SEG_ONEPASS_BITS64 9                 // binary64 rows: one pass up to 2^this partitions (wide above 2^8)
+#define SEG_ONEPASS_BITS64 10                // binary64 rows: one pass up to 2^this partitions (wide above 2^8)
 #endif
 #ifndef SEG_ONEPASS_BITS32
 #define SEG_ONEPASS_BITS32 10                // binary32 rows (wide scatter above 2^8)

@@ -433,8 +433,9 @@ PART_CASES = [
     (np.float32, 1, 40000, 300000, 30),
     (np.float64, 4, 2049, 100000, 200),
     # partition-pass plans (k_partition.cu make_plan): P = ceil(G / 1024)
-    (np.float64, 3, (1 << 18) + 5, 600011, 30),   # P = 257: binary64 two passes (5 + 4 digit bits)
-    (np.float64, 2, (1 << 20) - 3, 700001, 20),   # P = 1024: two passes of 5 bits
+    (np.float64, 3, (1 << 18) + 5, 600011, 30),   # P = 257: binary64 one wide pass (512 digits)
+    (np.float64, 2, (1 << 20) - 3, 700001, 20),   # P = 1024: binary64 one wide pass (1024 digits)
+    (np.float64, 2, (1 << 21) + 3, 500003, 20),   # P = 2049: binary64 two passes (6 + 6)
     (np.float32, 2, (1 << 19) + 1, 600001, 20),   # P = 513: binary32 one wide pass (1024 digits)
     (np.float32, 2, (1 << 21) + 7, 500003, 10),   # P = 2049: binary32 two passes (6 + 6)
 ]

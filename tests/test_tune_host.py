@@ -14,7 +14,7 @@ def restore():
 
 
 def test_defaults():
-    assert R.tune_get(3, R.F64)["onepass_bits"] == 9
+    assert R.tune_get(3, R.F64)["onepass_bits"] == 10
     assert R.tune_get(2, R.F32)["onepass_bits"] == 10
 
 
