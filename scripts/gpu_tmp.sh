@@ -1,6 +1,11 @@
 cd $GRAFT_REPO_ROOT
-O=gpurun_out/sweep2; mkdir -p $O; : > $O/sweep_c2.jsonl
-for G in 1 4 16 64 256 1024 4096 16384 65536 262144 1048576 4194304 16777216; do
-  timeout 600 python bench.py --config 2 --n-groups $G --steps 20 --warmup 3 --no-e2e --no-cpu-baseline >> $O/sweep_c2.jsonl 2>> $O/sweep_c2.err
+for rep in 1 2; do
+for v in r7 r8; do
+REPRO_B200_LIB=$PWD/scripts/variants/lib_$v.so timeout 900 python bench.py --steps 200 --warmup 5 --no-e2e --no-cpu-baseline --no-parity --no-atomic-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c1 $v', round(d['ms_per_step'],4), round(d['roofline']['frac'],3))"
 done
-wc -l $O/sweep_c2.jsonl
+done
+for v in r7 r8; do
+for G in 32 4096; do
+REPRO_B200_LIB=$PWD/scripts/variants/lib_$v.so timeout 900 python bench.py --config 2 --n-groups $G --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-atomic-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('c2 $G $v', round(d['ms_per_step'],4))"
+done
+done
