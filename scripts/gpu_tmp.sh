@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out/final2
-timeout 3000 python -m pytest tests -m gpu -q -x > gpurun_out/final2/pytest_gpu.txt 2>&1; tail -2 gpurun_out/final2/pytest_gpu.txt
-timeout 600 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/final2/smoke.txt 2>&1; tail -2 gpurun_out/final2/smoke.txt
-timeout 900 python bench.py > gpurun_out/final2/bench_c1.json 2> gpurun_out/final2/bench_c1.err; head -c 300 gpurun_out/final2/bench_c1.json
+mkdir -p gpurun_out/lean16
+CMD="python bench.py --config 2 --n-groups 16 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-atomic-baseline"
+$CMD > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:lean -s 2 -c 1 -o gpurun_out/lean16/full $CMD > gpurun_out/lean16/ncu.log 2>&1
+tail -1 gpurun_out/lean16/ncu.log
