@@ -1,5 +1,3 @@
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out/lean16
-CMD="python bench.py --config 2 --n-groups 16 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-parity --no-atomic-baseline"
-$CMD > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:lean -s 2 -c 1 -o gpurun_out/lean16/full $CMD > gpurun_out/lean16/ncu.log 2>&1
-tail -1 gpurun_out/lean16/ncu.log
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_multi.py -q -x -k "lean or variant or few or config4 or moments or random" 2>&1 | tail -2
+for G in 1 16; do timeout 600 python bench.py --config 2 --n-groups $G --steps 20 --warmup 3 --no-e2e --no-cpu-baseline --no-atomic-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($G, round(d['ms_per_step'],4), d['parity']['vs_oracle'], round(d['roofline']['frac'],3), d['roofline']['kernel'])"; done
