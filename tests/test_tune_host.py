@@ -32,3 +32,10 @@ def test_invalid(restore, args):
     with pytest.raises(R.ReproError) as e:
         R.tune_set(*args)
     assert e.value.status == R.EINVAL
+
+
+def test_autotune_rejects_bad_arguments_before_any_device_work():
+    for args in ((1000, 3, R.F64), (1 << 20, 0, R.F64), (1 << 20, 3, 9)):
+        with pytest.raises(R.ReproError) as e:
+            R.autotune(*args)
+        assert e.value.status == R.EINVAL
