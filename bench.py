@@ -74,7 +74,7 @@ def parse():
 
 
 def shape(args):
-    from paper_1802_09883_b200 import synth
+    from inputs import synth
     if args.config in ARRAY:
         return args.rows or ARRAY[args.config]["n"], 1, 3, "f64"
     c = synth.CONFIGS[args.config]
@@ -85,7 +85,7 @@ def shape(args):
 
 def host_rows(config, r0, n, G):
     """Host copy of rows [r0, r0+n) of a config (numpy generator)."""
-    from paper_1802_09883_b200 import synth
+    from inputs import synth
     if config in ARRAY:  # values of config 1 (x) and of a second seed (y); no keys
         cols = [synth.generate(1, n=n, r0=r0)[1]]
         if ARRAY[config]["dot"]:
@@ -118,7 +118,7 @@ def device_rows(R, torch, config, r0, n, G):
     """Device-resident rows: generated on the GPU where the device generator
     exists (configs 0/1/2/4, bit-identical to synth.py), else uploaded."""
     if config in ARRAY:
-        from paper_1802_09883_b200 import synth
+        from inputs import synth
         cols = [R.synth_generate(1, n, 1024, r0=r0)[1][0]]
         if ARRAY[config]["dot"]:
             cols.append(R.synth_generate(1, n, 1024, r0=r0, seed=synth.SEED_BASE + config)[1][0])
@@ -228,6 +228,20 @@ def cpu_baseline(args, n, G, K):
                       f"{threads} host threads)", "seconds": t}
 
 
+def repo_libs_mapped():
+    """Shared objects under the repo root mapped into this process."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as fh:
+            for ln in fh:
+                path = ln.split()[-1] if len(ln.split()) >= 6 else ""
+                if path.endswith(".so") and path.startswith(ROOT):
+                    libs.add(os.path.relpath(path, ROOT))
+    except OSError:
+        return None
+    return sorted(libs)
+
+
 def reference_arm(args):
     """--impl reference: the CPU oracle as it stands, timed on the host cores
     (rank 0 only; other ranks exit without work).  Each step is a bounded
@@ -266,6 +280,9 @@ def reference_arm(args):
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": "oracle",
                          "sample": f"{sample} consecutive rows of the workload per step"},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # shared objects of this repo mapped into the arm's process: the oracle
+        # only (the arm never imports the product package)
+        "repo_libs_mapped": repo_libs_mapped(),
     }
     print(json.dumps(line), flush=True)
     return 0

@@ -138,6 +138,18 @@ def _dev(t, name, dtype=None):
     return t.data_ptr() if t.numel() else None
 
 
+def _need(t, n: int, name: str):
+    """The C-ABI cannot see buffer sizes: check them here (ValueError, not a
+    device out-of-bounds access)."""
+    if t is not None and t.numel() < n:
+        raise ValueError(f"{name} has {t.numel()} elements, needs >= {n}")
+
+
+def _same_len(a, b, what: str = "keys and vals"):
+    if a.numel() != b.numel():
+        raise ValueError(f"{what} differ in length")
+
+
 def _stream_ptr(stream):
     torch = _torch()
     if stream is None:
@@ -149,10 +161,10 @@ def groupby_sum(keys, vals, n_groups: int, fold: int = 3, out=None):
     """Reproducible GroupBy-SUM (blocking).  keys int32[n], vals f32/f64[n] on CUDA."""
     torch = _torch()
     dt = _dtype_code(vals)
-    if keys.numel() != vals.numel():
-        raise ValueError("keys and vals differ in length")
+    _same_len(keys, vals)
     if out is None:
         out = torch.empty(n_groups, dtype=vals.dtype, device=vals.device)
+    _need(out, n_groups, "out")
     st = _lib.repro_groupby_sum(_dev(keys, "keys", torch.int32), _dev(vals, "vals"), keys.numel(),
                                 n_groups, fold, dt, _dev(out, "out", vals.dtype))
     _check(st, "repro_groupby_sum")
@@ -181,6 +193,9 @@ def groupby_sum_async(keys, vals, n_groups: int, fold: int, out, workspace, stat
     workspace (make_workspace) and an int32 device status word."""
     torch = _torch()
     dt = _dtype_code(vals)
+    _same_len(keys, vals)
+    _need(out, n_groups, "out")
+    _need(status, 1, "status")
     wp, wb = _aligned_ptr(workspace)
     st = _lib.repro_groupby_sum_async(_dev(keys, "keys", torch.int32), _dev(vals, "vals"), keys.numel(), n_groups,
                                       fold, dt, _dev(out, "out", vals.dtype), wp, wb, _stream_ptr(stream),
@@ -198,8 +213,12 @@ def groupby_sum_host(keys, vals, n_groups: int, fold: int = 3, out=None):
     if keys.dtype != torch.int32:
         raise TypeError("keys must be int32")
     dt = _dtype_code(vals)
+    _same_len(keys, vals)
     if out is None:
         out = torch.empty(n_groups, dtype=vals.dtype)
+    _need(out, n_groups, "out")
+    if out.is_cuda or out.dtype != vals.dtype or not out.is_contiguous():
+        raise TypeError("out must be a contiguous host tensor of the value dtype")
     st = _lib.repro_groupby_sum_host(keys.data_ptr() if keys.numel() else None,
                                      vals.data_ptr() if vals.numel() else None, keys.numel(), n_groups, fold,
                                      dt, out.data_ptr())
@@ -216,9 +235,14 @@ def _multi_args(keys, cols, n_groups, proj, outs, counts):
     for c in cols:
         if c.dtype != cols[0].dtype or c.numel() != n:
             raise ValueError("value columns must share dtype and length with keys")
-    nout = 4 if proj == 1 else len(cols)
+    nout = 4 if proj == 1 else 2 if proj == 2 else len(cols)
     if outs is None:
         outs = [torch.empty(n_groups, dtype=cols[0].dtype, device=cols[0].device) for _ in range(nout)]
+    if len(outs) < nout:
+        raise ValueError(f"{nout} output columns needed, got {len(outs)}")
+    for o in outs:
+        _need(o, n_groups, "outs[i]")
+    _need(counts, n_groups, "counts")
     cptr = (_vp * len(cols))(*[_dev(c, "cols") for c in cols])
     optr = (_vp * len(outs))(*[_dev(o, "outs", cols[0].dtype) for o in outs])
     cnt = _dev(counts, "counts", torch.int64) if counts is not None else None
@@ -278,6 +302,7 @@ def sum(x, fold: int = 3, out=None):  # noqa: A001 -- the paper's operation name
     dt = _dtype_code(x)
     if out is None:
         out = torch.empty(1, dtype=x.dtype, device=x.device)
+    _need(out, 1, "out")
     _check(_lib.repro_sum(_dev(x, "x"), x.numel(), fold, dt, _dev(out, "out", x.dtype)), "repro_sum")
     return out
 
@@ -290,6 +315,7 @@ def dot(x, y, fold: int = 3, out=None):
         raise ValueError("x and y differ in length")
     if out is None:
         out = torch.empty(1, dtype=x.dtype, device=x.device)
+    _need(out, 1, "out")
     _check(_lib.repro_dot(_dev(x, "x"), _dev(y, "y", x.dtype), x.numel(), fold, dt, _dev(out, "out", x.dtype)),
            "repro_dot")
     return out
@@ -305,6 +331,8 @@ def dot_async(x, y, fold: int, out, workspace, status, stream=None):
     dt = _dtype_code(x)
     if y is not None and y.numel() != x.numel():
         raise ValueError("x and y differ in length")
+    _need(out, 1, "out")
+    _need(status, 1, "status")
     wp, wb = _aligned_ptr(workspace)
     st = _lib.repro_dot_async(_dev(x, "x"), None if y is None else _dev(y, "y", x.dtype), x.numel(), fold, dt,
                               _dev(out, "out", x.dtype), wp, wb, _stream_ptr(stream),
@@ -343,6 +371,7 @@ def dot_deposit_async(x, y, fold: int, workspace, stream=None):
 
 def dot_finish_async(fold: int, dtype: int, out, workspace, status, stream=None):
     torch = _torch()
+    _need(out, 1, "out")
     wp, wb = _aligned_ptr(workspace)
     _check(_lib.repro_dot_finish_async(fold, dtype, _dev(out, "out"), wp, wb, _stream_ptr(stream),
                                        _dev(status, "status", torch.int32)), "repro_dot_finish_async")
@@ -384,6 +413,7 @@ def groupby_sum_multi_async(keys, cols, n_groups: int, fold: int, proj: int, out
                             stream=None):
     torch = _torch()
     dt, n, outs, cptr, optr, cnt = _multi_args(keys, cols, n_groups, proj, outs, counts)
+    _need(status, 1, "status")
     wp, wb = _aligned_ptr(workspace)
     st = _lib.repro_groupby_sum_multi_async(_dev(keys, "keys", torch.int32), cptr, len(cols), proj, n, n_groups,
                                             fold, dt, optr, cnt, wp, wb, _stream_ptr(stream),
@@ -396,7 +426,7 @@ def synth_generate(config: int, n: int, n_groups: int, r0: int = 0, seed: int | 
     """Seeded synthetic inputs of BASELINE config 0/1/2/4 generated on the
     device (same bits as synth.generate); returns (keys, [value columns])."""
     torch = _torch()
-    from .synth import SEED_BASE
+    from inputs.synth import SEED_BASE
     seed = SEED_BASE + config if seed is None else seed
     keys = torch.empty(n, dtype=torch.int32, device="cuda")
     cols = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(4 if config == 4 else 1)]
@@ -453,6 +483,8 @@ def baseline_atomic_sum(keys, vals, n_groups: int, variant: int = 0, accumulate_
     odt = torch.float64 if (dt == F64 or accumulate_f64) else torch.float32
     if out is None:
         out = torch.empty(n_groups, dtype=odt, device=vals.device)
+    _same_len(keys, vals)
+    _need(out, n_groups, "out")
     st = _lib.repro_baseline_atomic_sum(_dev(keys, "keys", torch.int32), _dev(vals, "vals"), keys.numel(), n_groups,
                                         dt, variant, 1 if accumulate_f64 else 0, _dev(out, "out", odt),
                                         _stream_ptr(stream))
@@ -517,6 +549,7 @@ class Accumulator:
         torch = _torch()
         if _dtype_code(vals) != self.dtype:
             raise TypeError("value dtype does not match the accumulator")
+        _same_len(keys, vals)
         _check(_lib.repro_acc_deposit(self._h, _dev(keys, "keys", torch.int32), _dev(vals, "vals"), keys.numel()),
                "repro_acc_deposit")
         return self
@@ -529,6 +562,7 @@ class Accumulator:
         torch = _torch()
         if out is None:
             out = torch.empty(self.n_groups, dtype=self._torch_dtype, device="cuda")
+        _need(out, self.n_groups, "out")
         _check(_lib.repro_acc_finalize(self._h, _dev(out, "out", self._torch_dtype)), "repro_acc_finalize")
         return out
 
@@ -536,10 +570,12 @@ class Accumulator:
         torch = _torch()
         if state is None:
             state = torch.empty(self.n_groups * 2 * self.fold, dtype=self._torch_dtype, device="cuda")
+        _need(state, self.n_groups * 2 * self.fold, "state")
         _check(_lib.repro_acc_export(self._h, _dev(state, "state", self._torch_dtype)), "repro_acc_export")
         return state
 
     def import_(self, state):
+        _need(state, self.n_groups * 2 * self.fold, "state")
         _check(_lib.repro_acc_import(self._h, _dev(state, "state", self._torch_dtype)), "repro_acc_import")
         return self
 
@@ -551,6 +587,7 @@ class Accumulator:
         torch = _torch()
         if out is None:
             out = torch.empty(self.n_groups, dtype=torch.int32, device="cuda")
+        _need(out, self.n_groups, "k")
         _check(_lib.repro_acc_top_levels(self._h, _dev(out, "k", torch.int32)), "repro_acc_top_levels")
         return out
 
@@ -558,6 +595,8 @@ class Accumulator:
         torch = _torch()
         if limbs is None:
             limbs = torch.empty(self.n_groups * self.fold * 2, dtype=torch.int64, device="cuda")
+        _need(k_global, self.n_groups, "k_global")
+        _need(limbs, self.n_groups * self.fold * 2, "limbs")
         _check(_lib.repro_acc_window_export(self._h, _dev(k_global, "k_global", torch.int32),
                                             _dev(limbs, "limbs", torch.int64)), "repro_acc_window_export")
         return limbs
@@ -565,6 +604,10 @@ class Accumulator:
     def window_import(self, k_global, limbs, g0: int = 0, count: int | None = None):
         torch = _torch()
         count = self.n_groups - g0 if count is None else count
+        if g0 < 0 or count < 0 or g0 + count > self.n_groups:
+            raise ValueError("group range outside the accumulator")
+        _need(k_global, count, "k_global")
+        _need(limbs, count * self.fold * 2, "limbs")
         _check(_lib.repro_acc_window_import_range(self._h, g0, count, _dev(k_global, "k_global", torch.int32),
                                                   _dev(limbs, "limbs", torch.int64)),
                "repro_acc_window_import_range")

@@ -793,8 +793,10 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         // is deposited without per-row checks.  One barrier decides it for the
         // whole block (and orders the previous tile's deposits before a fold).
         if (ONCHIP_FAST && !small_g) {
+            // bit 0: this thread's rows need the generic code; bit 1: a counter
+            // neared 2^30 (dynamic fold).  The row checks run whatever bit 1
+            // says: a pending fold must not let a bad row through the fast path.
             int slow = kuni < 0 || rem < TILE - tid;
-            slow |= (int)(big >> 31) << 1;  // bit 1: a counter neared 2^30 (dynamic fold)
             if (!slow) {
                 // k*(b) <= kuni  <=>  |b| < 2^(W kuni + W - 1 - m): compare the
                 // magnitude bits (sign shifted out); NaN/Inf fail it too
@@ -810,6 +812,7 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                 }
                 slow = (hwmax >= lim) | (kmax >= (uint32_t)G);
             }
+            slow |= (int)(big >> 31) << 1;
             const int any_flags = __syncthreads_or(slow);
             const int any_slow = any_flags & 1;
             refill();

@@ -4,7 +4,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1802_09883_b200 as R
-from paper_1802_09883_b200 import synth
+from inputs import synth
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 27
 keys = torch.empty(n, dtype=torch.int32, device="cuda")

@@ -10,7 +10,7 @@ CHILD = r'''
 import sys, numpy as np, torch
 sys.path.insert(0, %r)
 import oracle as O, paper_1802_09883_b200 as R
-from paper_1802_09883_b200 import synth
+from inputs import synth
 res = []
 for cfg, n, G in ((0, 1 << 16, 16), (1, 1 << 22, 1024), (1, 1 << 24, 1024), (1, 1 << 22, 3000),
                   ("hot", 1 << 22, 1024), ("hot", 1 << 22, 16), ("hotneg", 1 << 22, 1024)):

@@ -6,7 +6,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import oracle as O
 import paper_1802_09883_b200 as R
-from paper_1802_09883_b200 import synth
+from inputs import synth
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 22
 G = int(sys.argv[2]) if len(sys.argv) > 2 else 1024
 k, v = synth.generate(1, n=n, n_groups=G)

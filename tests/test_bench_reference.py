@@ -28,3 +28,7 @@ def test_reference_arm_prints_the_contract_line(config):
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert "workload" in d["config"]
+    # the oracle arm never maps the product library
+    assert d["repo_libs_mapped"] is not None
+    assert not any("librepro_b200" in p for p in d["repo_libs_mapped"]), d["repo_libs_mapped"]
+    assert any("liboracle" in p for p in d["repo_libs_mapped"]), d["repo_libs_mapped"]

@@ -16,7 +16,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import oracle as O  # noqa: E402  (test infrastructure)
-from paper_1802_09883_b200 import synth  # noqa: E402
+from inputs import synth  # noqa: E402
 
 
 @pytest.fixture(scope="module")

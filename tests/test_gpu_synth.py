@@ -7,7 +7,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-from paper_1802_09883_b200 import synth  # noqa: E402
+from inputs import synth  # noqa: E402
 
 
 @pytest.fixture(scope="module")

@@ -7,7 +7,7 @@ from fractions import Fraction
 import numpy as np
 
 import oracle as O
-from paper_1802_09883_b200 import synth
+from inputs import synth
 
 
 def rn64(q: Fraction) -> float:

@@ -550,3 +550,107 @@ def test_groupby_matches_closed_form_per_group():
             v = [float(x) for x in vals[keys == g]]
             ktop, T = X.state_closed_form(v, K, BITS[dtype])
             assert bits64(float(out[g])) == bits64(X.finalize_closed_form(ktop, T, BITS[dtype]))
+
+
+# --------------------------------------------------------------------------
+# edge values: window thresholds, subnormals, signed zeros, half-unit ties
+# (Alg. 1 line 3 PAPER.md:660; readings A-1, A-9, A-11), pinned against the
+# exact-rational closed form
+# --------------------------------------------------------------------------
+
+import edge_values as EV  # noqa: E402
+
+
+@pytest.mark.parametrize("bits,K", [(64, 2), (64, 3), (32, 2), (32, 3)])
+def test_edge_values_closed_form(bits, K):
+    rng = np.random.default_rng(900 + bits + K)
+    dtype = F64 if bits == 64 else F32
+    p = O.params(dtype, K)
+    for ktop in (0, 1, 2, FMT_KMAX[bits]):
+        pool = EV.edge_pool(bits, K, ktop)
+        # every value on its own, then random multisets
+        sets = [[v] for v in pool] + [list(rng.choice(pool, int(rng.integers(2, 30)))) for _ in range(60)]
+        for vals in sets:
+            vals = [float(v) for v in vals]
+            st = O.deposit_all(p, vals)
+            ktop_cf, T = X.state_closed_form(vals, K, bits)
+            S, C = X.canonical_SC(ktop_cf, T, bits)
+            assert st.S == S and st.C == C, (vals, st, S, C)
+            assert bits64(O.finalize(p, st)) == bits64(X.finalize_closed_form(ktop_cf, T, bits)), vals
+
+
+FMT_KMAX = {64: 25, 32: 7}
+
+
+@pytest.mark.parametrize("bits", [64, 32])
+def test_edge_erange_limit(bits):
+    # |b| >= 2^(W KMAX + W - 1 - m) needs a non-finite extractor (reading A-9)
+    dtype = np.float64 if bits == 64 else np.float32
+    lim = EV.erange_limit(bits)
+    assert lim == (2.0 ** 987 if bits == 64 else 2.0 ** 120)
+    k = np.zeros(3, np.int32)
+    for K in (1, 2, 3):
+        assert O.groupby_sum(k, np.array([1.0, lim, 2.0], dtype), 1, K)[0] == O.ERANGE
+        assert O.groupby_sum(k, np.array([1.0, -lim, 2.0], dtype), 1, K)[0] == O.ERANGE
+        rc, out = O.groupby_sum(k, np.array([0.0, EV.below(lim, bits), 0.0], dtype), 1, K)
+        assert rc == O.OK
+        if K >= 2:  # the value's bits span two levels: a single value round-trips
+            assert float(out[0]) == EV.below(lim, bits)
+
+
+def test_subnormals_and_signed_zero_give_positive_zero():
+    # f = 0: subnormals lie below every ulp of the k = 0 window and contribute
+    # nothing (reading A-11); zeros of either sign give +0.0
+    for bits, dtype in ((64, np.float64), (32, np.float32)):
+        vals = np.array(EV.subnormals(bits), dtype)
+        for K in (1, 2, 3, 4):
+            rc, out = O.groupby_sum(np.zeros(vals.size, np.int32), vals, 1, K)
+            assert rc == O.OK and out.tobytes() == np.zeros(1, dtype).tobytes()
+
+
+def test_half_unit_ties_round_away_from_zero():
+    # (d + 1/2) u_1 at the top level of the k = 1 window: digit d + 1 (away
+    # from zero) and remainder -u_1/2, i.e. digit -2^(W-1) at the next level
+    # (reading A-1); hand-derived digits, then the oracle's state against them
+    for bits, K in ((64, 2), (32, 2)):
+        m, W, _ = EV.FMT[bits]
+        dtype = F64 if bits == 64 else F32
+        p = O.params(dtype, K)
+        for d in (0, 1, 2, 7):
+            for sgn in (1, -1):
+                v = sgn * (d + 0.5) * 2.0 ** (W - m)
+                T = [sgn * (d + 1), -sgn * (1 << (W - 1))]
+                assert X.state_closed_form([v], K, bits) == (1, T)
+                S, C = X.canonical_SC(1, T, bits)
+                st = O.deposit_all(p, [v])
+                assert st.S == S and st.C == C, (v, st, S, C)
+
+
+# --------------------------------------------------------------------------
+# binary32 carry counter limit (reading A-8): |C| >= 2^24 is ERANGE
+# --------------------------------------------------------------------------
+
+def test_f32_carry_limit_crafted_state():
+    # canonical k = 0 state, D = 0: t_1 = 0.25 ufp C = C / 4 (exact for |C| < 2^24)
+    p = O.params(F32, 2)
+    for c in (2.0 ** 24, -(2.0 ** 24), 2.0 ** 24 + 2.0):
+        with pytest.raises(ValueError, match=str(O.ERANGE)):
+            O.finalize(p, O.State([1.5, 1.5 * 2.0 ** -18], [c, 0.0]))
+    for c in (2.0 ** 24 - 1, -(2.0 ** 24 - 1), 12345.0):
+        q = O.finalize(p, O.State([1.5, 1.5 * 2.0 ** -18], [c, 0.0]))
+        assert q == float(np.float32(c / 4))
+
+
+def test_f32_carry_limit_by_deposits():
+    # b = the largest binary32 below 2^-6 has level-1 digit 2^17 at window 0:
+    # n rows carry C_1 = n 2^17 / 2^21 = n / 16.  n = 2^28 reaches C = 2^24.
+    b = np.float32(EV.below(2.0 ** -6, 32))
+    assert float(b) == 2.0 ** -6 - 2.0 ** -30
+    n = 1 << 28
+    keys = np.zeros(n, np.int32)
+    vals = np.full(n, b, np.float32)
+    assert O.groupby_sum(keys, vals, 1, 2)[0] == O.ERANGE
+    m = n - 16  # C = 2^24 - 1: readable; all value bits lie above ulp_2, so Q = RN(exact)
+    rc, out = O.groupby_sum(keys[:m], vals[:m], 1, 2)
+    exact = Fraction(m) * Fraction(float(b))
+    assert rc == O.OK and float(out[0]) == X.round_to_binary(exact, 32) == 2.0 ** 22 - 0.5
