@@ -70,6 +70,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-atomic-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="headline workload only (skip the sub-results)")
     return ap.parse_args()
 
 
@@ -288,6 +289,254 @@ def reference_arm(args):
     return 0
 
 
+# ---- one workload: timed steps, per-kernel roofline, baselines, parity ----------
+
+CONFIG2_GROUPS = [16, 1024, 4096, 1 << 16, 1 << 20, 1 << 24]  # sub-results of the default run
+
+
+def oracle_parity(R, torch, config, keys, cols, host, G, K, outs, counts):
+    """Bit comparison of the GPU outputs with the oracle on the SAME input
+    bytes (D2H copies of the device rows, or the host rows they came from).
+    Full comparison where the oracle finishes in seconds; 258 sampled groups
+    recomputed one by one at G > 2^20; config 4 streamed in shards of 2^26
+    rows whose oracle states are merged with the oracle's own merge (O3)."""
+    import oracle as O
+    thr = O.default_threads()
+    if config in ARRAY:
+        hc = host[1] if host else [c.cpu().numpy() for c in cols]
+        rc, ref, _ = oracle_run(config, None, hc, G, K, thr)
+        ok = rc == 0 and outs[0].cpu().numpy().tobytes() == ref[0].tobytes()
+        return {"vs_oracle": "bit-exact" if ok else "MISMATCH", "rows_compared": int(hc[0].size)}
+    if config == 4:
+        n = keys.numel()
+        p = O.params(O.F64, K)
+        states = [[None] * G for _ in range(4)]
+        cnt = np.zeros(G, np.int64)
+        sh = 1 << 26
+        for a in range(0, n, sh):
+            b = min(n, a + sh)
+            hk = keys[a:b].cpu().numpy()
+            hc = [c[a:b].cpu().numpy() for c in cols]
+            dp, ch = O.q1_project(hc[1], hc[2], hc[3])
+            for j, c in enumerate([hc[0], hc[1], dp, ch]):
+                rc, _, st = O.groupby_sum(hk, c, G, K, threads=thr, with_state=True)
+                if rc != 0:
+                    return {"vs_oracle": f"oracle status {rc}", "rows_compared": n}
+                for g in range(G):
+                    s_ = O.State(list(st[g, :K]), list(st[g, K:]))
+                    if states[j][g] is None:
+                        states[j][g] = s_
+                    elif O.merge(p, states[j][g], s_) != 0:
+                        return {"vs_oracle": "oracle merge error", "rows_compared": n}
+            cnt += np.bincount(hk[(hk >= 0) & (hk < G)], minlength=G)
+        ok = np.array_equal(counts.cpu().numpy(), cnt)
+        for j in range(4):
+            ref = np.array([O.finalize(p, states[j][g]) for g in range(G)], np.float64)
+            ok = ok and outs[j].cpu().numpy().tobytes() == ref.tobytes()
+        return {"vs_oracle": "bit-exact" if ok else "MISMATCH", "groups": G, "rows_compared": n, "columns": 4,
+                "counts": True, "oracle_shards": -(-n // sh)}
+    hk = host[0] if host else keys.cpu().numpy()
+    hv = host[1][0] if host else cols[0].cpu().numpy()
+    got = outs[0].cpu().numpy()
+    if G <= (1 << 20):
+        rc, ref = O.groupby_sum(hk, hv, G, K, threads=thr)
+        ok = rc == 0 and got.tobytes() == ref.tobytes()
+        return {"vs_oracle": "bit-exact" if ok else "MISMATCH", "groups": G, "rows_compared": int(hk.size)}
+    rng = np.random.default_rng(0)
+    sel = np.unique(np.concatenate([[0, G - 1], rng.integers(0, G, 256)])).astype(np.int32)
+    rc, ref = O.groupby_sum_select(hk, hv, G, K, sel, threads=thr)
+    ok = rc == 0 and got[sel].tobytes() == ref.tobytes()
+    return {"vs_oracle": "bit-exact" if ok else "MISMATCH", "groups_sampled": int(sel.size),
+            "rows_compared": int(hk.size)}
+
+
+def run_workload(R, torch, args, config, n, G, K, dts, world, rank, local, steps, warmup, *, parity=True,
+                 atomic=True, headline=False):
+    """Time the whole hot path on one workload; returns the result dict."""
+    import torch.distributed as dist
+    from paper_1802_09883_b200 import dist as rdist
+    dt = R.F64 if dts == "f64" else R.F32
+    vsz = 8 if dt == R.F64 else 4
+    multi = config == 4
+    array = config in ARRAY
+    ncol = 4 if multi else (2 if array and ARRAY[config]["dot"] else 1)
+    row_bytes = (0 if array else 4) + ncol * vsz
+    host = None
+    if config == 3:  # transcendental values: generated on the host, uploaded
+        hk, hc = host_rows(config, rank * n, n, G)
+        host = (hk, hc)
+        keys, cols = torch.from_numpy(hk).cuda(), [torch.from_numpy(c).cuda() for c in hc]
+    else:
+        keys, cols = device_rows(R, torch, config, rank * n, n, G)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    counts = None
+    if array:
+        outs = [torch.empty(1, dtype=cols[0].dtype, device="cuda")]
+        ws = R.make_dot_workspace(K, dt)
+        ycol = cols[1] if ncol == 2 else None
+    elif multi:
+        outs = [torch.empty(G, dtype=torch.float64, device="cuda") for _ in range(4)]
+        counts = torch.empty(G, dtype=torch.int64, device="cuda")
+        ws = R.make_multi_workspace(n, G, 4, 1, K, dt)
+    else:
+        outs = [torch.empty(G, dtype=cols[0].dtype, device="cuda")]
+        ws = R.make_workspace(n, G, K, dt)
+    acc = R.Accumulator(G, K, dt) if (world > 1 and not multi and not array) else None
+
+    def step():
+        if array:
+            if world == 1:
+                R.dot_async(cols[0], ycol, K, outs[0], ws, status, stream)
+            else:  # deposit, all-reduce the integer slot table, read out on every rank
+                rdist.dot_dist(R, cols[0], ycol, K, outs[0], ws, status, stream=stream)
+            return
+        if multi:
+            if world == 1:
+                R.groupby_sum_multi_async(keys, cols, G, K, 1, outs, counts, ws, status, stream)
+            else:  # deposit, all-reduce the integer slot tables, read out on every rank
+                rdist.groupby_sum_multi_dist(R, keys, cols, G, K, 1, outs, counts, ws, status, stream=stream)
+            return
+        if world == 1:
+            R.groupby_sum_async(keys, cols[0], G, K, outs[0], ws, status, stream)
+            return
+        acc.reset()
+        acc.deposit(keys, cols[0])
+        if G >= 4096:  # reduce-scatter by group range + all-gather of the results
+            rdist.reduce_scatter_finalize(acc, outs[0])
+        else:
+            rdist.allreduce_state(acc)
+            acc.finalize(outs[0])
+
+    for _ in range(max(warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    if int(status.item()) != 0:
+        raise SystemExit(f"device status {status.item()} in warm-up ({WORKLOADS.get(config)}, G={G})")
+
+    def timed_region(per_kernel):
+        R.timing_enable(per_kernel)
+        R.timing_collect()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(local) as clk:
+            ev0.record(stream)
+            for _ in range(steps):
+                step()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        R.timing_enable(False)
+        pk = R.timing_collect()
+        ms = ev0.elapsed_time(ev1)
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        return ms, pk, clk.result()
+
+    # region A: the step as a user runs it (no per-kernel events) -> value
+    ms, _, clocks = timed_region(False)
+    st_a = int(status.item())
+    # region B: the same steps with every library kernel bracketed by events
+    # on its stream -> per-kernel times and the dominant kernel's roofline
+    ms_b, per_kernel, _ = timed_region(True)
+    st_b = int(status.item())
+    ms_per_step = ms / steps
+    rows_total = n * world
+    value = rows_total / (ms_per_step * 1e-3)
+    peak, peak_src = peaks()
+    dom = max(per_kernel.items(), key=lambda kv: kv[1][1]) if per_kernel else None
+    roof = None
+    if dom:
+        name, (cnt, kms) = dom
+        avg_ms = kms / cnt
+        alg_bytes = n * row_bytes  # the kernel's algorithmic input bytes per launch (DESIGN.md 7)
+        achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": name, "kernel_ms": avg_ms,
+                "kernel_share_of_step": kms / ms_b if ms_b else None, "alg_bytes_per_launch": alg_bytes,
+                "alg_bytes_per_row": row_bytes, "peak_source": peak_src,
+                "traffic_note": "DRAM bytes per launch from ncu --set full: profiles/r2_*_ncu_full.txt"}
+    step_bytes = n * row_bytes + G * vsz * (5 if multi else 1)
+    res = {
+        "workload": WORKLOADS.get(config), "config": config, "rows_per_gpu": n, "n_groups": G, "fold": K,
+        "dtype": dts, "ms_per_step": ms_per_step, "value": value, "unit": "rows/s",
+        "step_hbm_gbs": step_bytes / (ms_per_step * 1e-3) / 1e9,
+        "step_roofline_frac": (step_bytes / (ms_per_step * 1e-3) / 1e9) / peak,
+        "roofline": roof, "per_kernel_ms": {k: v[1] / v[0] for k, v in per_kernel.items()},
+        "gpu_launches": sum(c for c, _ in per_kernel.values()), "path": R.last_path(), "clocks": clocks,
+        "device_status_after_timed_steps": st_a if st_a else st_b,
+    }
+    if st_a or st_b:
+        res["rejected"] = f"device status {st_a or st_b} during the timed steps"
+
+    # non-reproducible atomicAdd GroupBy on the same GPU and the same rows:
+    # the fastest of the four variants (global RED per row, shared-memory
+    # table, register partials for <= 16 groups, warp aggregation of equal keys)
+    if atomic and world == 1 and not multi and not array:
+        best = None
+        for variant in (0, 1, 2, 3):
+            try:
+                for _ in range(3):
+                    R.baseline_atomic_sum(keys, cols[0], G, variant=variant, stream=stream)
+                torch.cuda.synchronize()
+                b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                bsteps = max(5, steps // 2)
+                b0.record(stream)
+                for _ in range(bsteps):
+                    R.baseline_atomic_sum(keys, cols[0], G, variant=variant, stream=stream)
+                b1.record(stream)
+                torch.cuda.synchronize()
+                bms = b0.elapsed_time(b1) / bsteps
+                if best is None or bms < best[1]:
+                    best = (variant, bms)
+            except R.ReproError:
+                continue
+        if best:
+            names = ["global_atomicAdd", "smem_privatised_atomicAdd", "register_partials_atomicAdd",
+                     "warp_aggregated_atomicAdd"]
+            res["baseline_atomic"] = {"variant": names[best[0]], "ms_per_step": best[1],
+                                      "rows_per_s": n / (best[1] * 1e-3),
+                                      "slowdown_repro_vs_atomic": ms_per_step / best[1]}
+
+    if headline and not args.no_e2e and world == 1 and not multi and not array:
+        kp = keys.cpu().pin_memory()
+        vp = cols[0].cpu().pin_memory()
+        R.groupby_sum_host(kp, vp, G, K)
+        e2e_steps = max(3, min(steps, 10))
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            r_ = R.groupby_sum_host(kp, vp, G, K)
+        et = (time.perf_counter() - t0) / e2e_steps
+        kd2, vd2 = torch.empty_like(keys), torch.empty_like(cols[0])
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            kd2.copy_(kp, non_blocking=True)
+            vd2.copy_(vp, non_blocking=True)
+        torch.cuda.synchronize()
+        h2d = 3 * n * row_bytes / (time.perf_counter() - t0) / 1e9
+        del kd2, vd2
+        res["e2e"] = {"value": n / et, "unit": "rows/s", "h2d_bytes_per_step": n * row_bytes,
+                      "d2h_bytes_per_step": G * vsz, "ms_per_step": et * 1e3, "steps": e2e_steps,
+                      "h2d_copy_gbs": h2d, "e2e_gbs": n * row_bytes / et / 1e9,
+                      "bit_identical_to_device_path": bool(torch.equal(r_, outs[0].cpu()))}
+        del kp, vp
+
+    if parity and rank == 0 and world == 1 and not args.no_parity:
+        t0 = time.perf_counter()
+        res["parity"] = oracle_parity(R, torch, config, keys, cols, host, G, K, outs, counts)
+        res["parity"]["seconds"] = time.perf_counter() - t0
+    del keys, cols, ws, outs, acc
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -305,207 +554,36 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     n, G, K, dts = shape(args)
-    dt = R.F64 if dts == "f64" else R.F32
-    vsz = 8 if dt == R.F64 else 4
-    multi = args.config == 4
-    array = args.config in ARRAY
-    ncol = 4 if multi else (2 if array and ARRAY[args.config]["dot"] else 1)
-    row_bytes = (0 if array else 4) + ncol * vsz
-    keys, cols = device_rows(R, torch, args.config, rank * n, n, G)
-    torch.cuda.synchronize()
-    stream = torch.cuda.current_stream()
-    status = torch.zeros(1, dtype=torch.int32, device="cuda")
-    if array:
-        out = torch.empty(1, dtype=torch.float64, device="cuda")
-        ws = R.make_dot_workspace(K, dt)
-        ycol = cols[1] if ncol == 2 else None
-    elif multi:
-        outs = [torch.empty(G, dtype=torch.float64, device="cuda") for _ in range(4)]
-        counts = torch.empty(G, dtype=torch.int64, device="cuda")
-        ws = R.make_multi_workspace(n, G, 4, 1, K, dt)
-    else:
-        out = torch.empty(G, dtype=cols[0].dtype, device="cuda")
-        ws = R.make_workspace(n, G, K, dt)
-
-    from paper_1802_09883_b200 import dist as rdist
-    acc = R.Accumulator(G, K, dt) if (world > 1 and not multi and not array) else None
-
-    def step():
-        if array:
-            if world == 1:
-                R.dot_async(cols[0], ycol, K, out, ws, status, stream)
-            else:  # deposit, all-reduce the integer slot table, read out on every rank
-                rdist.dot_dist(R, cols[0], ycol, K, out, ws, status, stream=stream)
-            return
-        if multi:
-            if world == 1:
-                R.groupby_sum_multi_async(keys, cols, G, K, 1, outs, counts, ws, status, stream)
-            else:  # deposit, all-reduce the integer slot tables, read out on every rank
-                rdist.groupby_sum_multi_dist(R, keys, cols, G, K, 1, outs, counts, ws, status, stream=stream)
-            return
-        if world == 1:
-            R.groupby_sum_async(keys, cols[0], G, K, out, ws, status, stream)
-            return
-        acc.reset()
-        acc.deposit(keys, cols[0])
-        if G >= 4096:  # reduce-scatter by group range + all-gather of the results
-            rdist.reduce_scatter_finalize(acc, out)
-        else:
-            rdist.allreduce_state(acc)
-            acc.finalize(out)
-
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
-    if int(status.item()) != 0:
-        raise SystemExit(f"device status {status.item()}")
-
-    # ---- timed region ------------------------------------------------------
-    R.timing_enable(True)
-    R.timing_collect()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    R.timing_enable(False)
-    per_kernel = R.timing_collect()
-    ms = ev0.elapsed_time(ev1)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    launches = sum(c for c, _ in per_kernel.values())  # kernels of librepro_b200 in the timed region
-    ms_per_step = ms / args.steps
-    rows_total = n * world
-    value = rows_total / (ms_per_step * 1e-3)
-
-    # ---- dominant kernel roofline -----------------------------------------
-    peak, peak_src = peaks()
-    dom = max(per_kernel.items(), key=lambda kv: kv[1][1]) if per_kernel else None
-    roof = None
-    if dom:
-        name, (cnt, kms) = dom
-        avg_ms = kms / cnt
-        alg_bytes = n * row_bytes  # the kernel's algorithmic input bytes per launch
-        achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic(args.config), "kernel": name, "kernel_ms": avg_ms,
-                "kernel_share_of_step": kms / ms if ms else None, "alg_bytes_per_launch": alg_bytes,
-                "alg_bytes_per_row": row_bytes, "peak_source": peak_src}
-    step_bytes = n * row_bytes + G * vsz * (5 if multi else 1)
+    head = run_workload(R, torch, args, args.config, n, G, K, dts, world, rank, local, args.steps, args.warmup,
+                        headline=True)
     line = {
-        "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "metric": METRIC, "value": head["value"], "unit": "rows/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": head["ms_per_step"], "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": dts, "data": "synthetic",
         "config": {"workload": WORKLOADS.get(args.config), "rows_per_gpu": n, "n_groups": G, "fold": K,
                    "parallelism": f"dp{world}" if world > 1 else "single",
-                   "l2": f"inputs {n * row_bytes / 1e9:.2f} GB/GPU > 126 MB L2 (no flush needed)"},
-        "step_hbm_gbs": step_bytes / (ms_per_step * 1e-3) / 1e9,
-        "step_roofline_frac": (step_bytes / (ms_per_step * 1e-3) / 1e9) / peak,
-        "roofline": roof,
-        "per_kernel_ms": {k: v[1] / v[0] for k, v in per_kernel.items()},
-        "gpu_launches": launches,
-        "path": R.last_path(),
-        "clocks": clk.result(),
+                   "l2": f"inputs {n * (head['roofline'] or {}).get('alg_bytes_per_row', 12) / 1e9:.2f} GB/GPU "
+                         f"> 126 MB L2 (no flush needed)"},
     }
+    for k in ("step_hbm_gbs", "step_roofline_frac", "roofline", "per_kernel_ms", "gpu_launches", "path", "clocks",
+              "baseline_atomic", "e2e", "parity", "device_status_after_timed_steps", "rejected"):
+        if k in head:
+            line[k] = head[k]
 
-    # ---- non-reproducible atomicAdd baseline on the same GPU -------------------
-    if not args.no_atomic_baseline and world == 1 and not multi and not array:
-        best = None
-        for variant in (0, 1):
-            try:
-                for _ in range(3):
-                    R.baseline_atomic_sum(keys, cols[0], G, variant=variant, out=None, stream=stream)
-                torch.cuda.synchronize()
-                b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                bsteps = max(10, args.steps // 4)
-                b0.record(stream)
-                for _ in range(bsteps):
-                    R.baseline_atomic_sum(keys, cols[0], G, variant=variant, stream=stream)
-                b1.record(stream)
-                torch.cuda.synchronize()
-                bms = b0.elapsed_time(b1) / bsteps
-                if best is None or bms < best[1]:
-                    best = (variant, bms)
-            except R.ReproError:
-                continue
-        if best:
-            line["baseline_atomic"] = {"variant": ["global_atomicAdd", "smem_privatised_atomicAdd"][best[0]],
-                                       "ms_per_step": best[1], "rows_per_s": n / (best[1] * 1e-3),
-                                       "slowdown_repro_vs_atomic": ms_per_step / best[1]}
+    # the other BASELINE configs, measured in the same process (N = 1, default run)
+    if world == 1 and not args.no_configs and args.config == 1 and args.rows is None:
+        subs = {}
+        for g in CONFIG2_GROUPS:
+            subs[f"config2_G{g}"] = run_workload(R, torch, args, 2, 1 << 28, g, 3, "f64", world, rank, local,
+                                                 args.steps, args.warmup)
+        subs["config3"] = run_workload(R, torch, args, 3, 1 << 28, 1 << 20, 2, "f32", world, rank, local,
+                                       args.steps, args.warmup)
+        subs["config4"] = run_workload(R, torch, args, 4, 1 << 30, 4, 3, "f64", world, rank, local,
+                                       max(3, args.steps // 4), args.warmup)
+        line["configs"] = subs
 
-    # ---- end-to-end through the C-ABI with host buffers ---------------------
-    if not args.no_e2e and world == 1 and not multi and not array:
-        kp = keys.cpu().pin_memory()
-        vp = cols[0].cpu().pin_memory()
-        R.groupby_sum_host(kp, vp, G, K)
-        e2e_steps = max(3, min(args.steps, 10))
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            res = R.groupby_sum_host(kp, vp, G, K)
-        et = (time.perf_counter() - t0) / e2e_steps
-        # the PCIe ceiling for context: the same bytes, plain pinned H2D copies
-        kd2, vd2 = torch.empty_like(keys), torch.empty_like(cols[0])
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        for _ in range(3):
-            kd2.copy_(kp, non_blocking=True)
-            vd2.copy_(vp, non_blocking=True)
-        torch.cuda.synchronize()
-        h2d = 3 * n * row_bytes / (time.perf_counter() - t0) / 1e9
-        del kd2, vd2
-        line["e2e"] = {"value": n / et, "unit": "rows/s", "h2d_bytes_per_step": n * row_bytes,
-                       "d2h_bytes_per_step": G * vsz, "ms_per_step": et * 1e3, "steps": e2e_steps,
-                       "h2d_copy_gbs": h2d, "e2e_gbs": n * row_bytes / et / 1e9,
-                       "bit_identical_to_device_path": bool(torch.equal(res, out.cpu()))}
-        del kp, vp
-
-    # ---- oracle: cpu_baseline + parity ---------------------------------------
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, n, G, K)
-    if rank == 0 and world == 1 and not args.no_parity:
-        import oracle as O
-        if array:
-            _, hc = host_rows(args.config, 0, n, G)
-            rc, ref, _ = oracle_run(args.config, None, hc, G, K, O.default_threads())
-            got = out.cpu().numpy()
-            line["parity"] = {"vs_oracle": "bit-exact" if (rc == 0 and got.tobytes() == ref[0].tobytes())
-                              else "MISMATCH", "rows_compared": n}
-        elif multi:
-            # full-size run is compared on its leading rows: GPU and oracle both
-            # recompute rows [0, P) exactly
-            P = min(n, PARITY_ROWS_MULTI)
-            po, pc = R.groupby_sum_multi(keys[:P], [c[:P] for c in cols], G, K, proj=1)
-            hk, hc = host_rows(4, 0, P, G)
-            rc, ref, ref_counts = oracle_run(4, hk, hc, G, K, O.default_threads())
-            same = rc == 0 and all(o.cpu().numpy().tobytes() == r.tobytes() for o, r in zip(po, ref)) and \
-                np.array_equal(pc.cpu().numpy(), ref_counts)
-            line["parity"] = {"vs_oracle": "bit-exact" if same else "MISMATCH", "groups": G,
-                              "rows_compared": P, "columns": 4, "counts": True}
-        elif n <= (1 << 28) and G <= (1 << 16):
-            hk, hc = host_rows(args.config, 0, n, G)
-            rc, ref, _ = oracle_run(args.config, hk, hc, G, K, O.default_threads())
-            got = out.cpu().numpy()
-            line["parity"] = {"vs_oracle": "bit-exact" if (rc == 0 and got.tobytes() == ref[0].tobytes())
-                              else "MISMATCH", "groups": G, "rows_compared": n}
-        else:
-            # large G: sampled groups, recomputed one by one by the oracle
-            hk, hc = host_rows(args.config, 0, n, G)
-            rng = np.random.default_rng(0)
-            sel = np.unique(np.concatenate([[0, G - 1], rng.integers(0, G, 256)])).astype(np.int32)
-            rc, ref = O.groupby_sum_select(hk, hc[0], G, K, sel)
-            got = out.cpu().numpy()[sel]
-            line["parity"] = {"vs_oracle": "bit-exact" if (rc == 0 and got.tobytes() == ref.tobytes())
-                              else "MISMATCH", "groups_sampled": int(sel.size), "rows_compared": n}
-
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

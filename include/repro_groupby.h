@@ -362,9 +362,12 @@ int repro_acc_window_import_range(repro_acc *acc, int32_t g0, int32_t count,
  * out[g] = atomicAdd-accumulated sum in the value dtype (or in binary64 when
  * accumulate_f64 != 0 and dtype is F32).  variant 0: one global atomicAdd
  * per row; variant 1: shared-memory privatised table per block (compare-
- * and-swap on sm_100a) flushed with global atomics.  out is zeroed inside.
- * Stream-ordered, non-blocking; returns REPRO_EINVAL for bad arguments or
- * when variant 1 does not fit shared memory.
+ * and-swap on sm_100a) flushed with global atomics; variant 2 (n_groups <=
+ * 16): per-thread register partials, one global atomic per group per warp;
+ * variant 3: warp aggregation of equal keys (match.any), one global atomic
+ * per distinct key per warp.  out is zeroed inside.  Stream-ordered,
+ * non-blocking; returns REPRO_EINVAL for bad arguments or when the variant
+ * does not apply (1: shared memory too small, 2: n_groups > 16).
  * ---------------------------------------------------------------------- */
 int repro_baseline_atomic_sum(const int32_t *keys, const void *vals, int64_t n,
                               int32_t n_groups, int32_t dtype, int32_t variant,
@@ -381,16 +384,21 @@ int32_t repro_last_launch_count(void);
 int32_t repro_last_path(void);
 /* Largest n_groups the on-chip path handles for (fold, dtype). */
 int32_t repro_onchip_max_groups(int32_t fold, int32_t dtype);
-/* Force a path for testing: -1 auto (default), 0 on-chip, 1 partitioned.
- * Never changes result bits. */
+/* Largest n_groups the two-pass sweep (partitioned path 1) handles. */
+int32_t repro_sweep_max_groups(int32_t fold, int32_t dtype);
+/* Force a path for testing: -1 auto (default), 0 on-chip, 1 partitioned
+ * (the two-pass sweep where its 256 partitions suffice, else segmented radix
+ * passes), 2 partitioned by segmented radix passes.  repro_last_path reports
+ * the same numbers.  Never changes result bits. */
 void repro_set_path_override(int32_t path);
 
 /* Choose the on-chip accumulate kernel for testing: 0 auto (default: the
  * lean per-warp kernel for <= 16 groups single-column / <= 4 groups
  * multi-column, the keyless register kernel for repro_sum / repro_dot, else
- * the TMA-fed per-row shared-atomic kernel), 1 the per-row shared-atomic
- * kernel, 2 the tile-sorted kernel, 3 the per-row shared-atomic kernel with
- * register loads (no TMA).  Never changes result bits. */
+ * the register-fed counter-table kernel k_table), 1 the per-row
+ * shared-atomic kernel fed by a TMA ring, 2 k_table, 3 the per-row
+ * shared-atomic kernel with register loads (no TMA).  Never changes result
+ * bits. */
 void repro_set_kernel_variant(int32_t variant);
 
 /* Per-kernel device timing (benchmark aid).  While enabled, every kernel the

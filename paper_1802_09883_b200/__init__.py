@@ -90,6 +90,7 @@ _sig("repro_baseline_atomic_sum", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32
 _sig("repro_last_launch_count", _i32)
 _sig("repro_last_path", _i32)
 _sig("repro_onchip_max_groups", _i32, _i32, _i32)
+_sig("repro_sweep_max_groups", _i32, _i32, _i32)
 _sig("repro_set_path_override", None, _i32)
 _sig("repro_set_kernel_variant", None, _i32)
 _sig("repro_timing_enable", None, _i32)
@@ -504,12 +505,17 @@ def onchip_max_groups(fold: int, dtype: int) -> int:
     return _lib.repro_onchip_max_groups(fold, dtype)
 
 
+def sweep_max_groups(fold: int, dtype: int) -> int:
+    return _lib.repro_sweep_max_groups(fold, dtype)
+
+
 def set_path_override(path: int):
     _lib.repro_set_path_override(path)
 
 
 def set_kernel_variant(variant: int):
-    """0 auto, 1 per-row shared atomics, 2 tile-sorted runs (bits never change)."""
+    """0 auto, 1 per-row atomics fed by the TMA ring, 2 k_table (register-fed
+    counter table), 3 per-row atomics with register loads (bits never change)."""
     _lib.repro_set_kernel_variant(variant)
 
 

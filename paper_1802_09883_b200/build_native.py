@@ -42,9 +42,12 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     from concurrent.futures import ThreadPoolExecutor
     import tempfile
 
+    import time
+
     target = out or LIB
     if not force and out is None and not stale():
         return LIB
+    t_start = time.time()  # the library is stamped with this time: a source edited during the build stays newer
     os.makedirs(os.path.dirname(target), exist_ok=True)
     common = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"), "-I", CSRC]
     tmp = tempfile.mkdtemp(prefix="repro_build_")
@@ -71,6 +74,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
         sys.stderr.write("".join(r.stdout + r.stderr for r in failed))
         raise RuntimeError("nvcc failed building librepro_b200.so")
     os.replace(target + ".tmp", target)
+    os.utime(target, (t_start, t_start))
     if verbose:
         print("".join(r.stderr for r in results))
     return target

@@ -119,15 +119,19 @@ bool valid_shape(int32_t G, int32_t K, int32_t dt) {
     return G >= 1 && K >= 1 && K <= 4 && (dt == REPRO_F32 || dt == REPRO_F64);
 }
 
-// 0 = on-chip, 1 = partitioned, -1 = not supported
+// 0 = on-chip table, 1 = partitioned by the two-pass sweep (k_sweep.cu),
+// 2 = partitioned by segmented radix passes (k_partition.cu: group counts
+// beyond the sweep's 256 partitions), -1 = not supported
 int choose_path(int32_t G, int32_t K, int32_t dt) {
     int onchip = onchip_max_groups(K, dt);
     const int32_t cross = g_onchip_cross[dt == REPRO_F64][K];
     if (cross > 0 && g_path_override < 0) onchip = std::min<int>(onchip, cross);
+    const int part = G <= sweep_max_groups(K, dt) ? 1 : G <= partition_max_groups(K, dt) ? 2 : -1;
     if (g_path_override == 0) return G <= onchip ? 0 : -1;
-    if (g_path_override == 1) return G <= partition_max_groups(K, dt) ? 1 : -1;
+    if (g_path_override == 1) return part;
+    if (g_path_override == 2) return G <= partition_max_groups(K, dt) ? 2 : -1;
     if (G <= onchip) return 0;
-    return G <= partition_max_groups(K, dt) ? 1 : -1;
+    return part;
 }
 
 // on-chip workspace: [flags | kglob int32[G] | slots u64[G][NS][2]]
@@ -161,6 +165,7 @@ OnchipWs carve_onchip(void *ws, int64_t n, int32_t G, int32_t K, int32_t dt) {
 
 size_t ws_bytes_for(int path, int64_t n, int32_t G, int32_t K, int32_t dt) {
     if (path == 0) return onchip_ws_bytes(n, G, K, dt);
+    if (path == 1) return ALIGN + sweep_workspace_bytes(n, G, K, dt);
     return ALIGN + partition_workspace_bytes(n, G, K, dt);
 }
 
@@ -268,7 +273,10 @@ int enqueue_groupby(const int32_t *keys, const void *vals, int64_t n, int32_t G,
         OnchipWs w = carve_onchip(ws, n, G, K, dt);
         *flags_out = w.flags;
         if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return REPRO_ECUDA;
-        int rc = timed(lean_single_applies(keys, vals, G) ? "lean_single" : "onchip_accumulate", st, [&] {
+        const char *label = lean_single_applies(keys, vals, G) ? "lean_single"
+                            : (onchip_variant() == 1 || onchip_variant() == 3) ? "onchip_accumulate"
+                                                                                : "table_accumulate";
+        int rc = timed(label, st, [&] {
             return launch_onchip_any(dt, K, keys, vals, n, G, w.kglob, w.slots, w.flags, st, &t_launches);
         });
         if (rc) return map_launch(rc);
@@ -281,6 +289,9 @@ int enqueue_groupby(const int32_t *keys, const void *vals, int64_t n, int32_t G,
     uint32_t *flags = (uint32_t *)ws;
     *flags_out = flags;
     if (cudaMemsetAsync(flags, 0, ALIGN, st) != cudaSuccess) return REPRO_ECUDA;
+    if (path == 1)
+        return map_launch(launch_sweep(dt, K, keys, vals, n, G, (char *)ws + ALIGN, ws_bytes - ALIGN, merge, acc_k,
+                                       acc_C, acc_D, out, flags, st, &t_launches));
     int rc = launch_partitioned(dt, K, keys, vals, n, G, (char *)ws + ALIGN, ws_bytes - ALIGN, merge, acc_k,
                                 acc_C, acc_D, out, flags, st, &t_launches);
     return map_launch(rc);
@@ -325,6 +336,10 @@ int32_t repro_onchip_max_groups(int32_t fold, int32_t dtype) {
     if (fold < 1 || fold > 4 || (dtype != 0 && dtype != 1)) return 0;
     return onchip_max_groups(fold, dtype);
 }
+int32_t repro_sweep_max_groups(int32_t fold, int32_t dtype) {
+    if (fold < 1 || fold > 4 || (dtype != 0 && dtype != 1)) return 0;
+    return sweep_max_groups(fold, dtype);
+}
 void repro_set_kernel_variant(int32_t variant) { set_onchip_variant(variant); }
 
 void repro_timing_enable(int32_t on) { t_timing = on != 0; }
@@ -359,7 +374,7 @@ int32_t repro_timing_collect(const char **names, int32_t *counts, double *total_
     return k;
 }
 
-void repro_set_path_override(int32_t path) { g_path_override = (path == 0 || path == 1) ? path : -1; }
+void repro_set_path_override(int32_t path) { g_path_override = (path >= 0 && path <= 2) ? path : -1; }
 
 size_t repro_groupby_workspace_bytes(int64_t n, int32_t n_groups, int32_t fold, int32_t dtype) {
     if (n < 0 || !valid_shape(n_groups, fold, dtype)) return 0;
@@ -869,7 +884,8 @@ int repro_autotune(int64_t n, int32_t fold, int32_t dtype, int32_t *onchip_max_g
     size_t wsb = 0;
     for (int32_t G = 2048; G <= gmax; G *= 2)
         wsb = std::max(wsb, std::max(ws_bytes_for(0, n, std::min(G, cap), fold, dtype),
-                                     ws_bytes_for(1, n, G, fold, dtype)));
+                                     std::max(choose_path(G, fold, dtype) == 1 ? ws_bytes_for(1, n, G, fold, dtype) : 0,
+                                              ws_bytes_for(2, n, G, fold, dtype))));
     bool ok = cudaMalloc(&keys, 4 * (size_t)n) == cudaSuccess && cudaMalloc(&v64, 8 * (size_t)n) == cudaSuccess &&
               cudaMalloc(&out, vsz * (size_t)gmax) == cudaSuccess && cudaMalloc(&ws, wsb) == cudaSuccess;
     if (ok && dtype == REPRO_F32) ok = cudaMalloc(&vals, 4 * (size_t)n) == cudaSuccess;
@@ -923,11 +939,11 @@ int repro_autotune(int64_t n, int32_t fold, int32_t dtype, int32_t *onchip_max_g
             const int64_t G = (int64_t)1024 << b;
             if (G > gmax) break;
             if (!gen((int32_t)G)) { ok = false; break; }
-            g_path_override = 1;
+            g_path_override = 2;
             set_partition_onepass_bits(dt1, b);
-            one[b] = time_path((int32_t)G, 1);
+            one[b] = time_path((int32_t)G, 2);
             set_partition_onepass_bits(dt1, b - 1);
-            two[b] = time_path((int32_t)G, 1);
+            two[b] = time_path((int32_t)G, 2);
             if (tlog)
                 fprintf(stderr, "repro_autotune: G=%lld %d-bit ids: one pass %.3f ms, two passes %.3f ms\n",
                         (long long)G, b, one[b], two[b]);
@@ -1232,7 +1248,10 @@ int repro_baseline_atomic_sum(const int32_t *keys, const void *vals, int64_t n, 
     if (n < 0 || n_groups < 1 || (dtype != 0 && dtype != 1) || !out || (n > 0 && (!keys || !vals)))
         return REPRO_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    return map_launch(timed(variant == 0 ? "baseline_atomic_global" : "baseline_atomic_smem", st, [&] {
+    static const char *names[4] = {"baseline_atomic_global", "baseline_atomic_smem", "baseline_atomic_regs",
+                                   "baseline_atomic_match"};
+    if (variant < 0 || variant > 3) return REPRO_EINVAL;
+    return map_launch(timed(names[variant], st, [&] {
         return launch_baseline(dtype, variant, accumulate_f64, keys, vals, n, n_groups, out, st, &t_launches);
     }));
 }

@@ -22,12 +22,12 @@ inline int slot_count(int DT, int K) { return (DT == 1 ? 25 : 7) + K; }
 // ---- launchers (return 0 on success, -1 unsupported shape, -2 CUDA error) --
 int onchip_max_groups(int K, int DT);
 void set_onchip_variant(int v);
-int onchip_variant();  // 0 auto, 1 atomic, 2 sorted, 3 atomic + register loads
-int sorted_max_groups(int K, int DT);
+int onchip_variant();  // 0 auto, 1 atomic (TMA ring), 2 table (k_table.cu), 3 atomic + register loads
 int atomic_max_groups(int K, int DT);
-int launch_sorted_any(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
-                      int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
-                      int *launches);
+int table_max_groups(int K, int DT);
+int launch_table_any(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
+                     int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
+                     int *launches);
 int launch_atomic_any(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
                       int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
                       int *launches);
@@ -114,6 +114,13 @@ size_t partition_workspace_bytes(int64_t n, int32_t G, int K, int DT);
 int launch_partitioned(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
                        void *ws, size_t ws_bytes, int merge, int32_t *acc_k, int64_t *acc_C,
                        int64_t *acc_D, void *out, uint32_t *status, cudaStream_t st, int *launches);
+
+// ---- partitioned path: two-pass sweep (k_sweep.cu) ----------------------
+int sweep_max_groups(int K, int DT);
+size_t sweep_workspace_bytes(int64_t n, int32_t G, int K, int DT);
+int launch_sweep(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G, void *ws,
+                 size_t ws_bytes, int merge, int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *out,
+                 uint32_t *status, cudaStream_t st, int *launches);
 
 // ---- non-reproducible baseline --------------------------------------------
 int launch_baseline(int DT, int variant, int acc64, const int32_t *keys, const void *vals,

@@ -51,14 +51,16 @@ int atomic_max_groups(int K, int DT) {
     return (int)(((cap - 64 - 127) / per) & ~(size_t)3);
 }
 
-// variant: 0 = auto, 1 = atomic (TMA-fed where the columns are 16-B aligned),
-// 2 = sorted, 3 = atomic with register loads only.
-// Initialised from REPRO_ONCHIP_VARIANT, settable through the C-ABI.
+// variant: 0 = auto (k_lean for <= 16 groups, else k_table), 1 = the
+// per-row atomic kernel fed by the TMA ring (accumulate_range), 2 = k_table,
+// 3 = the per-row atomic kernel with register loads.  The bits never depend
+// on the variant.  Initialised from REPRO_ONCHIP_VARIANT, settable through
+// the C-ABI.
 static int g_variant = -1;
 int onchip_variant() {
     if (g_variant < 0) {
         const char *e = getenv("REPRO_ONCHIP_VARIANT");
-        g_variant = (e && e[0] == 'a') ? 1 : (e && e[0] == 's') ? 2 : (e && e[0] == 'r') ? 3 : 0;
+        g_variant = (e && e[0] == 'a') ? 1 : (e && e[0] == 't') ? 2 : (e && e[0] == 'r') ? 3 : 0;
     }
     return g_variant;
 }
@@ -67,28 +69,24 @@ void set_onchip_variant(int v) { g_variant = (v >= 0 && v <= 3) ? v : 0; }
 int onchip_max_groups(int K, int DT) {
     const int v = onchip_variant();
     if (v == 1 || v == 3) return atomic_max_groups(K, DT);
-    if (v == 2) return sorted_max_groups(K, DT);
-    return std::max(atomic_max_groups(K, DT), sorted_max_groups(K, DT));
+    return table_max_groups(K, DT);
 }
 
 int launch_onchip_any(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
                       int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
                       int *launches) {
-    // auto (0): the per-row atomic kernel wherever it fits (measured faster at
-    // every group count on B200); the tile-sorted kernel only when asked for
-    // or when G exceeds the atomic kernel's capacity.
     // a handful of groups: per-warp lane-copy tables (k_lean.cu); 1 = not taken
     const int lr = launch_lean_single(DT, K, keys, vals, n, G, kglob, slots, status, st, launches);
     if (lr != 1) return lr;
     const int v = onchip_variant();
-    const bool sorted = (v == 2 && G <= sorted_max_groups(K, DT)) || G > atomic_max_groups(K, DT);
-    if (sorted) return launch_sorted_any(DT, K, keys, vals, n, G, kglob, slots, status, st, launches);
-    return launch_atomic_any(DT, K, keys, vals, n, G, kglob, slots, status, st, launches);
+    if (v == 1 || v == 3) return launch_atomic_any(DT, K, keys, vals, n, G, kglob, slots, status, st, launches);
+    return launch_table_any(DT, K, keys, vals, n, G, kglob, slots, status, st, launches);
 }
 
 int launch_atomic_any(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G,
                       int32_t *kglob, unsigned long long *slots, uint32_t *status, cudaStream_t st,
                       int *launches) {
+    if (G > atomic_max_groups(K, DT)) return -1;
 #define ONCHIP_CASE(dt, k) \
     if (DT == dt && K == k) return launch_onchip<dt, k>(keys, vals, n, G, kglob, slots, status, st, launches);
     ONCHIP_CASE(1, 1) ONCHIP_CASE(1, 2) ONCHIP_CASE(1, 3) ONCHIP_CASE(1, 4)

@@ -123,6 +123,25 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// Bitwise OR of v over the block; also a full barrier.  __syncthreads_or only
+// says whether ANY thread's predicate was non-zero (it returns 1, not the OR
+// of the values), so multi-bit flags go through a shared word.  Three words
+// rotate: the word of call c + 1 is cleared in call c, after every thread
+// has read it in call c - 2 (before the barrier of call c - 1).
+struct BlockOr {
+    int *w;    // 3 shared words, zeroed before the first call (and a barrier)
+    int call;  // calls so far (block-uniform)
+    __device__ __forceinline__ int operator()(int v) {
+        const int p = call % 3;
+        if (threadIdx.x == 0) w[(p + 1) % 3] = 0;
+        v = __reduce_or_sync(0xffffffffu, v);
+        if ((threadIdx.x & 31) == 0 && v) atomicOr(&w[p], v);
+        __syncthreads();
+        ++call;
+        return *(volatile int *)&w[p];
+    }
+};
+
 // Limbs of one row's K digits, computed from the bits (common.cuh digits_of
 // written out so that no 64-bit integer arithmetic is needed).
 //   binary64: the extractor is M' = 1.5*2^52 + 2^19, so t = x (+) M' has the
@@ -628,6 +647,9 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         }
     };
     set_count_limbs(0);
+    __shared__ int s_or3[3];
+    if (tid < 3) s_or3[tid] = 0;
+    BlockOr block_or{s_or3, 0};
     __syncthreads();
     // block-uniform window top: when every group has the same top `kuni`,
     // rows need no per-group lookup (the common case after the first tiles);
@@ -813,7 +835,7 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
                 slow = (hwmax >= lim) | (kmax >= (uint32_t)G);
             }
             slow |= (int)(big >> 31) << 1;
-            const int any_flags = __syncthreads_or(slow);
+            const int any_flags = block_or(slow);
             const int any_slow = any_flags & 1;
             refill();
             if (!any_slow) {
@@ -892,7 +914,7 @@ __device__ __forceinline__ void accumulate_range(const int32_t *__restrict__ key
         }
         // dynamic mode: every deposit is observed; fold when a counter was
         // seen at |old| >= 2^30 (bit 1 of the barrier's OR)
-        const int any_flags = __syncthreads_or(changed | (int)(big >> 31) << 1);  // + previous tile done
+        const int any_flags = block_or(changed | (int)(big >> 31) << 1);  // + previous tile done
         const int any = any_flags & 1;
         const bool fold = dyn ? (any_flags & 2) != 0 : since + VTILE > Cfg::LIMIT;
         if (!(ONCHIP_FAST && !small_g)) refill();

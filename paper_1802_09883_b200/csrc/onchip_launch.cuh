@@ -14,7 +14,7 @@
 
 namespace repro {
 
-int onchip_variant();  // k_onchip.cu: 0 auto, 1 atomic, 2 sorted, 3 atomic + register loads
+int onchip_variant();  // k_onchip.cu: 0 auto, 1 atomic (TMA ring), 2 table, 3 atomic + register loads
 
 template <int DT, int K, bool REGTOT, bool TMA, class SRC>
 __global__ void __launch_bounds__(256, ONCHIP_MINBLOCKS)

@@ -1,0 +1,365 @@
+// table_core.cuh -- the block-wide limb-counter table behind k_table (the
+// on-chip GroupBy, k_table.cu) and the partitioned path's sweep and
+// per-partition accumulation (k_sweep.cu).  See k_table.cu for the design:
+// word-major 32-bit limb counters in shared memory, one window top per
+// group, every level sum published into the ABSOLUTE-LEVEL slot table
+// (counter drains at |old| >= 2^29, demotions, the final flush), a
+// block-synchronous mode until every group shares one window top and a
+// barrier-free streaming mode after it.
+#pragma once
+
+#include "common.cuh"
+#include "onchip_core.cuh"
+
+namespace repro {
+
+constexpr uint32_t TAB_DRAIN_BIAS = 0x20000000u;  // |old| >= 2^29  <=>  (old + 2^29) has bit 30 or 31
+constexpr uint32_t TAB_DRAIN_MASK = 0xC0000000u;
+constexpr int TAB_MM = 32;  // shared control words of a Table (>= KMAX + 3)
+
+template <int DT>
+struct QuadT;
+template <>
+struct QuadT<1> {
+    int4 k;
+    double2 a, b;
+    __device__ __forceinline__ double v(int u) const { return u == 0 ? a.x : u == 1 ? a.y : u == 2 ? b.x : b.y; }
+};
+template <>
+struct QuadT<0> {
+    int4 k;
+    float4 a;
+    __device__ __forceinline__ float v(int u) const { return u == 0 ? a.x : u == 1 ? a.y : u == 2 ? a.z : a.w; }
+};
+__device__ __forceinline__ int kq(const int4 &k, int u) { return u == 0 ? k.x : u == 1 ? k.y : u == 2 ? k.z : k.w; }
+
+// 4 rows from row r (VEC: 16-byte streaming loads; else scalar)
+template <int DT, bool VEC>
+__device__ __forceinline__ void load_quad(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals,
+                                          int64_t r, QuadT<DT> &q) {
+    if (VEC) {
+        q.k = __ldcs(reinterpret_cast<const int4 *>(keys + r));
+        if constexpr (DT == 1) {
+            q.a = __ldcs(reinterpret_cast<const double2 *>(vals + r));
+            q.b = __ldcs(reinterpret_cast<const double2 *>(vals + r) + 1);
+        } else {
+            q.a = __ldcs(reinterpret_cast<const float4 *>(vals + r));
+        }
+    } else {
+        q.k = make_int4(__ldcs(keys + r), __ldcs(keys + r + 1), __ldcs(keys + r + 2), __ldcs(keys + r + 3));
+        if constexpr (DT == 1) {
+            q.a = make_double2(__ldcs(vals + r), __ldcs(vals + r + 1));
+            q.b = make_double2(__ldcs(vals + r + 2), __ldcs(vals + r + 3));
+        } else {
+            q.a = make_float4(__ldcs(vals + r), __ldcs(vals + r + 1), __ldcs(vals + r + 2), __ldcs(vals + r + 3));
+        }
+    }
+}
+// up to 4 rows (fewer at the end of a range), scalar loads; missing rows are
+// key 0, value 0
+template <int DT>
+__device__ __forceinline__ void load_partial(const int32_t *__restrict__ keys,
+                                             const typename Fmt<DT>::V *__restrict__ vals, int64_t r, int cnt,
+                                             QuadT<DT> &q) {
+    using V = typename Fmt<DT>::V;
+    int k[4] = {0, 0, 0, 0};
+    V v[4] = {V(0), V(0), V(0), V(0)};
+    for (int u = 0; u < cnt; ++u) { k[u] = keys[r + u]; v[u] = vals[r + u]; }
+    q.k = make_int4(k[0], k[1], k[2], k[3]);
+    if constexpr (DT == 1) { q.a = make_double2(v[0], v[1]); q.b = make_double2(v[2], v[3]); }
+    else q.a = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+__device__ __forceinline__ uint32_t atom_add_shared(uint32_t a, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ uint32_t atom_exch_shared(uint32_t a, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.exch.b32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+
+// Add a level sum T of group g at absolute level j into the slot table
+// (slot j + K - 1; low 32 bits and high part in separate 64-bit words, so
+// any number of partial sums adds without overflow).
+template <int DT, int K>
+__device__ __forceinline__ void slot_add(unsigned long long *slots, int64_t g, int j, int64_t T) {
+    constexpr int NS = Fmt<DT>::KMAX + K;
+    if (T == 0) return;
+    unsigned long long *p = slots + ((size_t)g * NS + (j + K - 1)) * 2;
+    atomicAdd(p, (unsigned long long)(T & 0xFFFFFFFFll));
+    atomicAdd(p + 1, (unsigned long long)(T >> 32));
+}
+
+// value of counter word w (level w / LIMBS, limb w % LIMBS) as a level-sum part
+template <int DT>
+__device__ __forceinline__ int64_t counter_part(int w, uint32_t c) {
+    if (Fmt<DT>::LIMBS == 2 && (w & 1)) return (int64_t)(int32_t)c * (int64_t)(1 << 20);
+    return (int64_t)(int32_t)c;
+}
+
+// Shared memory of a table of G groups: counters u32 [CW][gq], ktop int32
+// [gq], knext int32 [gq], raised-group list int32 [gq]; gq = G + 1 (a sink
+// group that receives the zero limbs of skipped rows) rounded to 4.
+template <int DT, int K>
+struct TabGeom {
+    static constexpr int LIMBS = Fmt<DT>::LIMBS;
+    static constexpr int CW = K * LIMBS;
+    __host__ __device__ static int gq(int G) { return (G + 1 + 3) & ~3; }
+    __host__ __device__ static size_t bytes(int G) { return (size_t)gq(G) * (4 * CW + 12); }
+};
+
+// One block's table.  Every method is entered by all threads of the block
+// (slow_quad and finish contain barriers; fast_quad is barrier-free).
+// GQC > 0: the counter-row stride is the compile-time constant GQC (>= gq(G)),
+// so every atomic's counter offset is an immediate.
+template <int DT, int K, int TPB, int GQC = 0>
+struct Table {
+    using F = Fmt<DT>;
+    using V = typename F::V;
+    using Geo = TabGeom<DT, K>;
+    static constexpr int CW = Geo::CW, LIMBS = Geo::LIMBS;
+
+    uint32_t *cnt;
+    int32_t *ktop, *knext;
+    int *s_mm;  // TAB_MM shared words: [0], [1] raised-group list lengths (by call parity), [2 + k] groups at top k
+    int32_t *rlist;  // raised groups of the current tile (shared, gq entries)
+    int G, gq;
+    int64_t gbase;  // global id of local group 0 (slot table / kglob index)
+    int32_t *kglob;
+    unsigned long long *slots;
+    uint32_t cbase, wstride;
+    int kuni;       // block-uniform window top (streaming mode) or -1
+    uint32_t lim;   // magnitude bits limit of kuni's window
+    uint32_t big;   // OR of (old + 2^29) over observed counters
+    bool first;
+    int par;  // parity of slow_quad calls (block-uniform)
+    Extractors<DT, K> ex;
+
+    __device__ __forceinline__ Table(unsigned char *mem, int *mm, int G_, int64_t gbase_, int32_t *kglob_,
+                                     unsigned long long *slots_)
+        : s_mm(mm), G(G_), gbase(gbase_), kglob(kglob_), slots(slots_), kuni(-1), lim(0), big(0), first(true),
+          par(0), ex(0) {
+        gq = GQC > 0 ? GQC : Geo::gq(G);
+        cnt = reinterpret_cast<uint32_t *>(mem);
+        ktop = reinterpret_cast<int32_t *>(cnt + (size_t)CW * gq);
+        knext = ktop + gq;
+        rlist = knext + gq;
+        cbase = (uint32_t)__cvta_generic_to_shared(cnt);
+        wstride = 4u * (uint32_t)gq;
+    }
+    // zero the table (caller: barrier before first use)
+    __device__ __forceinline__ void clear() {
+        for (int i = threadIdx.x; i < CW * gq; i += TPB) cnt[i] = 0;
+        for (int i = threadIdx.x; i < gq; i += TPB) { ktop[i] = 0; knext[i] = 0; }
+        for (int i = threadIdx.x; i < F::KMAX + 3; i += TPB) s_mm[i] = i == 2 ? G : 0;  // all G groups at top 0
+        kuni = -1;
+        par = 0;
+        lim = 0;
+        big = 0;
+        first = true;
+    }
+    __device__ __forceinline__ void drain(int g, int w, int kt) {
+        const uint32_t c = atom_exch_shared(cbase + 4u * (uint32_t)g + (uint32_t)w * wstride, 0u);
+        if (c) slot_add<DT, K>(slots, gbase + g, kt - w / LIMBS, counter_part<DT>(w, c));
+    }
+    // publish all counters of group g at window kt (no concurrent deposits)
+    __device__ __forceinline__ void publish_all(int g, int kt) {
+#pragma unroll
+        for (int l = 0; l < K; ++l) {
+            int64_t T = 0;
+#pragma unroll
+            for (int h = 0; h < LIMBS; ++h) {
+                const int w = l * LIMBS + h;
+                uint32_t *p = cnt + (size_t)w * gq + g;
+                T += counter_part<DT>(w, *p);
+                *p = 0;
+            }
+            slot_add<DT, K>(slots, gbase + g, kt - l, T);
+        }
+    }
+
+    // A row outside the streaming fast path: error bits, or (valid, k* above
+    // kuni) deposited at its own window straight into the slot table.
+    __device__ __forceinline__ void exceptional(int32_t k, V v, uint32_t &flags) {
+        uint32_t f = 0;
+        const int ks = kstar_of<DT>(v, f);
+        if ((uint32_t)k >= (uint32_t)G) { flags |= FLAG_EKEY; return; }
+        if (f) { flags |= f; return; }
+        typename F::Digit d[K];
+        digits_of<DT, K>(v, ks, d);
+        atomicMax(&kglob[gbase + k], ks);
+#pragma unroll
+        for (int l = 0; l < K; ++l) slot_add<DT, K>(slots, gbase + k, ks - l, (int64_t)d[l]);
+    }
+
+    // Streaming deposit of 4 rows under kuni (kuni >= 0).  `in` bit u: row u
+    // belongs to this table (others deposit zero limbs into the sink group).
+    // Rows that fail the key / window check are handled one by one.
+    __device__ __forceinline__ void fast_quad(const QuadT<DT> &q, uint32_t in, uint32_t &flags) {
+        int32_t key[4];
+        V val[4];
+        uint32_t exc = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int32_t k = kq(q.k, u);
+            const V v = q.v(u);
+            const uint32_t hw = DT == 1 ? (uint32_t)__double2hiint((double)v) << 1 : __float_as_uint((float)v) << 1;
+            const bool iu = (in >> u) & 1u;
+            const bool ok = iu && (uint32_t)k < (uint32_t)G && hw < lim;
+            exc |= (iu && !ok) ? 1u << u : 0u;
+            key[u] = ok ? k : G;  // sink group
+            val[u] = ok ? v : V(0);
+        }
+        uint32_t lo[4][K], hi[4][K], a[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            a[u] = cbase + 4u * (uint32_t)key[u];
+            if (DT == 1) {
+                double r = (double)val[u];
+#pragma unroll
+                for (int l = 0; l < K; ++l) {
+                    const double x = __hiloint2double(__double2hiint(r), __double2loint(r) | 1);  // reading A-1
+                    const double t = __dadd_rn(x, (double)ex.e[l]);
+                    const uint32_t tlo = (uint32_t)__double2loint(t);
+                    const uint32_t thi = (uint32_t)__double2hiint(t);
+                    lo[u][l] = (tlo & 0xFFFFFu) - 0x80000u;
+                    hi[u][l] = __funnelshift_r(tlo, thi, 20) - ex.eb[l];
+                    if (l + 1 < K) r = __dsub_rn(r, __dsub_rn(t, (double)ex.e[l]));
+                }
+            } else {
+                float r = (float)val[u];
+#pragma unroll
+                for (int l = 0; l < K; ++l) {
+                    const float x = __uint_as_float(__float_as_uint(r) | 1u);
+                    const float t = __fadd_rn(x, (float)ex.e[l]);
+                    lo[u][l] = __float_as_uint(t) - ex.eb[l];
+                    hi[u][l] = 0;
+                    if (l + 1 < K) r = __fsub_rn(r, __fsub_rn(t, (float)ex.e[l]));
+                }
+            }
+        }
+        // one atomic per counter position and row; positions the whole warp
+        // leaves at zero are skipped (one vote)
+#pragma unroll
+        for (int l = 0; l < K; ++l) {
+#pragma unroll
+            for (int h = 0; h < LIMBS; ++h) {
+                uint32_t any = 0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) any |= h ? hi[u][l] : lo[u][l];
+                if (__any_sync(0xffffffffu, any != 0u)) {
+                    const uint32_t off = (uint32_t)(LIMBS * l + h) * (GQC > 0 ? 4u * GQC : wstride);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) big |= atom_add_shared(a[u] + off, h ? hi[u][l] : lo[u][l]) + TAB_DRAIN_BIAS;
+                }
+            }
+        }
+        if (big & TAB_DRAIN_MASK) {  // rare: drain every counter of this batch that is past 2^29
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (key[u] >= G) continue;
+#pragma unroll
+                for (int w = 0; w < CW; ++w) {
+                    const uint32_t c = ld_shared_u32(a[u] + (uint32_t)w * wstride);
+                    if ((c + TAB_DRAIN_BIAS) & TAB_DRAIN_MASK) drain(key[u], w, kuni);
+                }
+            }
+            big = 0;
+        }
+        while (exc) {
+            const int u = __ffs(exc) - 1;
+            exc &= exc - 1;
+            exceptional(kq(q.k, u), q.v(u), flags);
+        }
+    }
+
+    // Block-synchronous deposit of 4 rows (row u taken when bit u of `in`):
+    // per-row k*, raise the groups' tops, publish a raised group's counters at
+    // its old window, then deposit each row at its group's window.  May switch
+    // the table to streaming mode (kuni >= 0, block-uniform).
+    __device__ __forceinline__ void slow_quad(const QuadT<DT> &q, uint32_t in, uint32_t &flags) {
+        const int tid = threadIdx.x;
+        int32_t key[4];
+        int changed = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            int ks;
+            key[u] = check_row<DT>(kq(q.k, u), q.v(u), (in >> u) & 1u, G, flags, ks);
+            if (key[u] >= 0 && ks > ktop[key[u]]) {
+                // the thread whose atomicMax first lifts knext above ktop lists the group
+                const int old = atomicMax(&knext[key[u]], ks);
+                if (old == ktop[key[u]]) rlist[atomicAdd(&s_mm[par], 1)] = key[u];
+                changed = 1;
+            }
+        }
+        const int any = __syncthreads_or(changed) | (first ? 1 : 0);
+        first = false;
+        // the other parity's list length was last read before the previous
+        // call's second barrier and is next appended to after this call's
+        if (tid == 0) s_mm[par ^ 1] = 0;
+        if (any) {
+            // raised groups only: publish at the old window, move the top, and
+            // keep the number of groups per window top (s_mm[1 + k])
+            const int nr = s_mm[par];
+            for (int i = tid; i < nr; i += TPB) {
+                const int g = rlist[i];
+                publish_all(g, ktop[g]);
+                atomicSub(&s_mm[2 + ktop[g]], 1);
+                atomicAdd(&s_mm[2 + knext[g]], 1);
+                ktop[g] = knext[g];
+            }
+            __syncthreads();
+            int ku = -1;
+            for (int k = 0; k <= F::KMAX; ++k)
+                if (s_mm[2 + k] == G) ku = k;
+            if (ku >= 0) {
+                kuni = ku;
+                ex = Extractors<DT, K>(kuni);
+                lim = (uint32_t)(F::W * kuni + F::W - 1 - F::m + F::BIAS) << (F::m % 32 + 1);
+            }
+        }
+        __syncthreads();  // raise phase done / the list length is reset before the next call's appends
+        par ^= 1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (key[u] < 0) continue;
+            const int kt = ktop[key[u]];
+            uint32_t lo[K], hi[K];
+            row_limbs<DT, K>(F::mul(q.v(u), F::pow2(F::m - F::W * kt)), lo, hi);
+            const uint32_t a = cbase + 4u * (uint32_t)key[u];
+#pragma unroll
+            for (int l = 0; l < K; ++l)
+#pragma unroll
+                for (int h = 0; h < LIMBS; ++h) {
+                    const uint32_t old = atom_add_shared(a + (uint32_t)(LIMBS * l + h) * wstride, h ? hi[l] : lo[l]);
+                    if ((old + TAB_DRAIN_BIAS) & TAB_DRAIN_MASK) drain(key[u], LIMBS * l + h, kt);
+                }
+        }
+    }
+
+    __device__ __forceinline__ void quad(const QuadT<DT> &q, uint32_t in, uint32_t &flags) {
+        if (kuni >= 0) fast_quad(q, in, flags);
+        else slow_quad(q, in, flags);
+    }
+
+    // publish every group's counters at its block window and raise the
+    // global tops; leaves the table zeroed (barriers on both sides)
+    __device__ __forceinline__ void finish() {
+        __syncthreads();
+        for (int g = threadIdx.x; g < G; g += TPB) {
+            publish_all(g, ktop[g]);
+            if (ktop[g] > 0) atomicMax(&kglob[gbase + g], ktop[g]);
+        }
+        __syncthreads();
+    }
+};
+
+}  // namespace repro

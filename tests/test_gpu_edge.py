@@ -164,25 +164,41 @@ def test_keyless_sum_edges(R, bits):
 # binary32 carry-count limit (reading A-8)
 # ---------------------------------------------------------------------------
 
+def _f32_state(cs):
+    # canonical k = 0 states with D = 0 and C_1 = c (SPEC.md:277 layout:
+    # S[0..K) then C[0..K) per group)
+    st = np.zeros((len(cs), 4), np.float32)
+    st[:, 0], st[:, 1] = 1.5, 1.5 * 2.0 ** -18
+    st[:, 2] = cs
+    return dev(st.reshape(-1))
+
+
 def test_f32_carry_limit_imported_state(R):
-    # canonical k = 0 state with D = 0 and C = c at level 1 (SPEC.md:277 layout
-    # S[0..K) then C[0..K)): readable for |c| < 2^24, ERANGE at 2^24
+    # |C| < 2^24 reads out C / 4; a merge that reaches |C| = 2^24 is ERANGE at
+    # read-out (reading A-8); importing |C| >= 2^24 is EINVAL (no canonical
+    # binary32 state the accumulator can export holds it)
+    cs = (2.0 ** 24 - 1, -(2.0 ** 24 - 1), 12345.0)
     acc = R.Accumulator(3, 2, R.F32)
-    for cs, ok in (((2.0 ** 24 - 1, -(2.0 ** 24 - 1), 12345.0), True), ((2.0 ** 24, 0.0, 0.0), False),
-                   ((0.0, -(2.0 ** 24), 0.0), False)):
-        st = np.zeros((3, 4), np.float32)
-        st[:, 0], st[:, 1] = 1.5, 1.5 * 2.0 ** -18
-        st[:, 2] = cs
-        acc.import_(dev(st.reshape(-1)))
-        if ok:
-            got = acc.finalize().cpu().numpy()
-            p = O.params(O.F32, 2)
-            ref = [O.finalize(p, O.State([1.5, 1.5 * 2.0 ** -18], [float(c), 0.0])) for c in cs]
-            assert got.tolist() == ref == [float(np.float32(c / 4)) for c in cs]
-        else:
-            with pytest.raises(R.ReproError) as e:
-                acc.finalize()
-            assert e.value.status == O.ERANGE
+    acc.import_(_f32_state(cs))
+    got = acc.finalize().cpu().numpy()
+    p = O.params(O.F32, 2)
+    ref = [O.finalize(p, O.State([1.5, 1.5 * 2.0 ** -18], [float(c), 0.0])) for c in cs]
+    assert got.tolist() == ref == [float(np.float32(c / 4)) for c in cs]
+    with pytest.raises(R.ReproError) as e:
+        acc.import_(_f32_state((2.0 ** 24, 0.0, 0.0)))
+    assert e.value.status == O.EINVAL
+    a, b = R.Accumulator(3, 2, R.F32), R.Accumulator(3, 2, R.F32)
+    a.import_(_f32_state((2.0 ** 23, -(2.0 ** 23), 2.0 ** 23 - 1)))
+    b.import_(_f32_state((2.0 ** 23, -(2.0 ** 23), 2.0 ** 23)))
+    a.merge(b)  # C = 2^24, -2^24, 2^24 - 1
+    with pytest.raises(R.ReproError) as e:
+        a.finalize()
+    assert e.value.status == O.ERANGE
+    # the oracle's merge of the same states agrees
+    sa, sb = O.State([1.5, 1.5 * 2.0 ** -18], [2.0 ** 23, 0.0]), O.State([1.5, 1.5 * 2.0 ** -18], [2.0 ** 23, 0.0])
+    assert O.merge(p, sa, sb) == O.OK
+    with pytest.raises(ValueError, match=str(O.ERANGE)):
+        O.finalize(p, sa)
 
 
 @pytest.mark.parametrize("path_kind", ["auto", "onchip", "partitioned"])

@@ -4,8 +4,7 @@ for bit (the type is associative, so the north star's bar is bit-exact).
 Sizes span several tiles (1792 rows per tile for binary64, 3840 for binary32,
 one tile per 256 x R rows) and ragged tails; the full BASELINE sizes are
 covered in test_gpu_full_size.py.  The `variant` fixture runs the on-chip
-cases under the TMA-fed kernel, the tile-sorted kernel and the register-load
-kernel (unaligned inputs take that path too).
+cases under k_table, the TMA-fed kernel and the register-load kernel (unaligned inputs take that path too).
 """
 import itertools
 
@@ -27,14 +26,18 @@ def R():
     return R
 
 
-@pytest.fixture(params=[0, 1, 2, 3], ids=["auto", "atomic", "sorted", "regload"])
+@pytest.fixture(params=[0, 1, 2, 3], ids=["auto", "atomic", "table", "regload"])
 def variant(R, request):
     """Run a test under each on-chip kernel (auto: the lean per-warp kernel for
-    <= 16 groups, else the TMA-fed per-row atomics / TMA-fed per-row atomics /
-    tile-sorted runs / per-row atomics with register loads)."""
+    <= 16 groups, else k_table / TMA-fed per-row atomics / k_table / per-row
+    atomics with register loads)."""
     R.set_kernel_variant(request.param)
     yield request.param
     R.set_kernel_variant(0)
+
+
+def dtype_code(dtype):
+    return 1 if dtype == np.float64 else 0
 
 
 def dev(a):
@@ -181,8 +184,6 @@ def test_single_row_round_trip(R, variant):
 def test_max_onchip_groups(R, variant):
     for dtype, K in ((np.float64, 3), (np.float32, 2)):
         G = R.onchip_max_groups(K, R.F64 if dtype == np.float64 else R.F32)
-        if variant == 2:  # the sorted kernel's own capacity
-            G = min(G, 2000 if dtype == np.float64 else 3000)
         assert G >= 1024
         rng = np.random.default_rng(G)
         n = 5 * G + 11
@@ -417,10 +418,13 @@ def test_atomic_baseline_close_to_repro(R):
 
 # ------------------------------------------------- partitioned path (row a5)
 
-@pytest.fixture
-def partitioned(R):
-    R.set_path_override(1)
-    yield
+@pytest.fixture(params=[1, 2], ids=["sweep", "segmented"])
+def partitioned(R, request):
+    """Force the partitioned path: 1 = the two-pass sweep (k_sweep.cu; beyond
+    its 256 partitions the segmented passes), 2 = the segmented radix passes
+    (k_partition.cu)."""
+    R.set_path_override(request.param)
+    yield request.param
     R.set_path_override(-1)
 
 
@@ -447,18 +451,22 @@ def test_partitioned_forced_matches_oracle(R, partitioned, dtype, K, G, n, sprea
     keys = rng.integers(0, G, n, dtype=np.int32)
     vals = mixed_values(rng, n, dtype, spread)
     got = gpu_groupby(R, keys, vals, G, K)
-    assert R.last_path() == 1
+    assert R.last_path() == (2 if partitioned == 2 or G > R.sweep_max_groups(K, dtype_code(dtype)) else 1)
     assert_bits_equal(got, oracle_groupby(keys, vals, G, K))
 
 
-@pytest.mark.parametrize("G", [5000, 1 << 17])
+@pytest.mark.parametrize("G", ["cap+1", 1 << 17, (1 << 20) + 5])
 def test_partitioned_auto_above_onchip_capacity(R, G):
+    # just above the on-chip table's capacity: the two-pass sweep (path 1);
+    # beyond the sweep's 256 partitions: segmented radix passes (path 2)
+    if G == "cap+1":
+        G = R.onchip_max_groups(3, R.F64) + 1
     rng = np.random.default_rng(G)
     n = 1 << 20
     keys = rng.integers(0, G, n, dtype=np.int32)
     vals = mixed_values(rng, n, np.float64, 25)
     got = gpu_groupby(R, keys, vals, G, 3)
-    assert R.last_path() == 1
+    assert R.last_path() == (1 if G <= (1 << 20) else 2)
     assert_bits_equal(got, oracle_groupby(keys, vals, G, 3))
 
 
