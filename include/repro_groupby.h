@@ -99,6 +99,63 @@ int repro_groupby_sum_host(const int32_t *keys_host, const void *vals_host,
 /* Free the internal workspace cache of the blocking entry points. */
 void repro_release_cache(void);
 
+/* Split form of repro_groupby_sum for several GPUs (SURVEY.md 8(e) steps
+ * 1-5), stream-ordered end to end (no host synchronisation); only for group
+ * counts the on-chip table or the two-pass sweep covers (n_groups <=
+ * repro_sweep_max_groups), else REPRO_EINVAL.  Workspace: as for
+ * repro_groupby_sum_async.
+ *  - repro_groupby_table: byte offsets (from the workspace start) and element
+ *    counts of the status word (uint32[1]), the global tops kglob (int32[G])
+ *    and the ABSOLUTE-LEVEL slot table (uint64[G][fold + 25 or + 7][2], used
+ *    as int64) that a deposit leaves in the workspace.
+ *  - repro_groupby_deposit_async: zero the table and deposit this rank's rows
+ *    (status bits EKEY/EDOM/ERANGE of the rows in the status word).
+ *  Exchange A (any n_groups): all-reduce the status word with bitwise OR
+ *  (e.g. MAX per bit), kglob with MAX and the slot table with SUM, then
+ *  repro_groupby_finish_async on every rank: Eq. 1 of every group into
+ *  out[n_groups], status into *d_status.
+ *  Exchange B (reduce-scatter by group range): all-reduce the status bits and
+ *  kglob (MAX); repro_groupby_window_limbs_async writes, per group, the fold
+ *  slot words under the global top k_global[g] (the paper's demotion,
+ *  PAPER.md:660-665, is a choice of slots) to limbs int64[G][fold][2]; the
+ *  caller reduce-scatters the limbs with SUM by contiguous group range and
+ *  each rank calls repro_groupby_finish_limbs_async for its range [g0, g0 +
+ *  count) (k_range = k_global + g0, limbs_range and out_range indexed from
+ *  g0); the caller all-gathers the outputs.  Integer SUM / MAX only, so the
+ *  bits equal repro_groupby_sum's for any rank count and reduction order. */
+int repro_groupby_table(int64_t n, int32_t n_groups, int32_t fold, int32_t dtype,
+                        int64_t *offsets, int64_t *counts);
+
+/* Exchange A through the switch (NVLS): the workspace
+ * lives in symmetric memory that every rank also maps at one MULTICAST
+ * address (mc_workspace: the multicast address of the 256-byte aligned
+ * workspace start).  offsets / counts: the 3 regions of repro_groupby_table
+ * (or repro_groupby_multi_table / repro_dot_table): status word, kglob,
+ * slots.  Rank `rank` of `world` reduces its 1/world slice of each region
+ * with multimem.ld_reduce (OR / MAX / integer ADD) and multimem-stores the
+ * result to every rank.  The caller brackets the call with barriers across
+ * the ranks (all deposits done before; all stores visible after), then
+ * finishes as for exchange A.  Stream-ordered. */
+int repro_nvls_table_allreduce_async(void *mc_workspace, const int64_t *offsets,
+                                     const int64_t *counts, int32_t rank,
+                                     int32_t world, void *stream);
+int repro_groupby_deposit_async(const int32_t *keys, const void *vals, int64_t n,
+                                int32_t n_groups, int32_t fold, int32_t dtype,
+                                void *workspace, size_t ws_bytes, void *stream);
+int repro_groupby_finish_async(int64_t n, int32_t n_groups, int32_t fold,
+                               int32_t dtype, void *out, void *workspace,
+                               size_t ws_bytes, void *stream, int32_t *d_status);
+int repro_groupby_window_limbs_async(int64_t n, int32_t n_groups, int32_t fold,
+                                     int32_t dtype, const int32_t *k_global,
+                                     int64_t *limbs, void *workspace,
+                                     size_t ws_bytes, void *stream);
+int repro_groupby_finish_limbs_async(int64_t n, int32_t n_groups, int32_t fold,
+                                     int32_t dtype, int32_t g0, int32_t count,
+                                     const int32_t *k_range,
+                                     const int64_t *limbs_range, void *out_range,
+                                     void *workspace, size_t ws_bytes,
+                                     void *stream, int32_t *d_status);
+
 /* Split form of the fused multi-column call for several GPUs (SURVEY.md
  * 8(e)); only for shapes the fused pass covers (n_groups * (outputs + 1) <=
  * 1024), else REPRO_EINVAL.  Each rank deposits its rows into the absolute-
@@ -303,7 +360,8 @@ int repro_acc_create(repro_acc **acc, int32_t n_groups, int32_t fold,
 int repro_acc_deposit(repro_acc *acc, const int32_t *keys, const void *vals,
                       int64_t n);
 
-/* dst += src (operator+=(repro)); same shape required. */
+/* dst += src (operator+=(repro)); same shape required;
+ * dst == src doubles the state. */
 int repro_acc_merge(repro_acc *dst, const repro_acc *src);
 
 /* out[g] = Eq. 1 read-out of every group (device array); non-mutating. */

@@ -46,6 +46,13 @@ _sig("repro_groupby_sum", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp)
 _sig("repro_groupby_workspace_bytes", _sz, _i64, _i32, _i32, _i32)
 _sig("repro_groupby_sum_async", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp)
 _sig("repro_groupby_sum_host", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp)
+_sig("repro_groupby_table", ctypes.c_int, _i64, _i32, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64))
+_sig("repro_nvls_table_allreduce_async", ctypes.c_int, _vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _i32, _i32, _vp)
+_sig("repro_groupby_deposit_async", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _sz, _vp)
+_sig("repro_groupby_finish_async", ctypes.c_int, _i64, _i32, _i32, _i32, _vp, _vp, _sz, _vp, _vp)
+_sig("repro_groupby_window_limbs_async", ctypes.c_int, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _sz, _vp)
+_sig("repro_groupby_finish_limbs_async", ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _sz,
+     _vp, _vp)
 _sig("repro_release_cache", None)
 _sig("repro_synth_generate", ctypes.c_int, _i32, ctypes.c_uint64, _i64, _i64, _i32, _vp, ctypes.POINTER(_vp), _vp)
 _sig("repro_groupby_sum_multi", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i32, _i64, _i32, _i32, _i32,
@@ -202,6 +209,89 @@ def groupby_sum_async(keys, vals, n_groups: int, fold: int, out, workspace, stat
                                       fold, dt, _dev(out, "out", vals.dtype), wp, wb, _stream_ptr(stream),
                                       _dev(status, "status", torch.int32))
     _check(st, "repro_groupby_sum_async")
+
+
+# ---- split form of the single-column GroupBy (multi-GPU exchange) --------------
+
+def groupby_table_views(workspace, n: int, n_groups: int, fold: int, dtype: int):
+    """(flags int32[1], kglob int32[G], slots int64[G * NS * 2]) views of the
+    absolute-level slot table a groupby_deposit_async leaves in `workspace`."""
+    torch = _torch()
+    off, cnt = (_i64 * 3)(), (_i64 * 3)()
+    _check(_lib.repro_groupby_table(n, n_groups, fold, dtype, off, cnt), "repro_groupby_table")
+    base = _aligned_ptr(workspace)[0] - workspace.data_ptr()
+    return tuple(workspace[base + o: base + o + c * sz].view(dt)
+                 for o, c, dt, sz in zip(off, cnt, (torch.int32, torch.int32, torch.int64), (4, 4, 8)))
+
+
+def table_layout(n: int, n_groups: int, fold: int, dtype: int):
+    """(offsets, counts) of the status word / kglob / slots regions of the
+    single-column slot table (bytes from the aligned workspace start)."""
+    off, cnt = (_i64 * 3)(), (_i64 * 3)()
+    _check(_lib.repro_groupby_table(n, n_groups, fold, dtype, off, cnt), "repro_groupby_table")
+    return list(off), list(cnt)
+
+
+def nvls_table_allreduce_async(mc_workspace: int, offsets, counts, rank: int, world: int, stream=None):
+    """In-switch all-reduce of a slot table through the multicast address of
+    the aligned workspace (repro_nvls_table_allreduce_async)."""
+    off, cnt = (_i64 * 3)(*offsets), (_i64 * 3)(*counts)
+    _check(_lib.repro_nvls_table_allreduce_async(mc_workspace, off, cnt, rank, world, _stream_ptr(stream)),
+           "repro_nvls_table_allreduce_async")
+
+
+def groupby_deposit_async(keys, vals, n_groups: int, fold: int, workspace, stream=None):
+    """Zero the workspace's slot table and deposit these rows into it."""
+    torch = _torch()
+    dt = _dtype_code(vals)
+    _same_len(keys, vals)
+    wp, wb = _aligned_ptr(workspace)
+    _check(_lib.repro_groupby_deposit_async(_dev(keys, "keys", torch.int32), _dev(vals, "vals"), keys.numel(),
+                                            n_groups, fold, dt, wp, wb, _stream_ptr(stream)),
+           "repro_groupby_deposit_async")
+
+
+def groupby_finish_async(n: int, n_groups: int, fold: int, dtype: int, out, workspace, status, stream=None):
+    """Eq. 1 read-out of every group from the (all-reduced) slot table."""
+    torch = _torch()
+    _need(out, n_groups, "out")
+    _need(status, 1, "status")
+    wp, wb = _aligned_ptr(workspace)
+    _check(_lib.repro_groupby_finish_async(n, n_groups, fold, dtype, _dev(out, "out"), wp, wb, _stream_ptr(stream),
+                                           _dev(status, "status", torch.int32)), "repro_groupby_finish_async")
+    return out
+
+
+def groupby_window_limbs_async(n: int, n_groups: int, fold: int, dtype: int, k_global, limbs, workspace,
+                               stream=None):
+    """limbs int64[G * fold * 2] <- the slot words under the global tops."""
+    torch = _torch()
+    _need(k_global, n_groups, "k_global")
+    _need(limbs, n_groups * fold * 2, "limbs")
+    wp, wb = _aligned_ptr(workspace)
+    _check(_lib.repro_groupby_window_limbs_async(n, n_groups, fold, dtype, _dev(k_global, "k_global", torch.int32),
+                                                 _dev(limbs, "limbs", torch.int64), wp, wb, _stream_ptr(stream)),
+           "repro_groupby_window_limbs_async")
+    return limbs
+
+
+def groupby_finish_limbs_async(n: int, n_groups: int, fold: int, dtype: int, g0: int, count: int, k_range,
+                               limbs_range, out_range, workspace, status, stream=None):
+    """Eq. 1 read-out of groups [g0, g0 + count) from summed limbs."""
+    torch = _torch()
+    if count:
+        _need(k_range, count, "k_range")
+        _need(limbs_range, count * fold * 2, "limbs_range")
+        _need(out_range, count, "out_range")
+    _need(status, 1, "status")
+    wp, wb = _aligned_ptr(workspace)
+    ptr = (lambda t, name, dt=None: _dev(t, name, dt) if count else None)
+    _check(_lib.repro_groupby_finish_limbs_async(n, n_groups, fold, dtype, g0, count,
+                                                 ptr(k_range, "k_range", torch.int32),
+                                                 ptr(limbs_range, "limbs_range", torch.int64),
+                                                 ptr(out_range, "out_range"), wp, wb, _stream_ptr(stream),
+                                                 _dev(status, "status", torch.int32)),
+           "repro_groupby_finish_limbs_async")
 
 
 def groupby_sum_host(keys, vals, n_groups: int, fold: int = 3, out=None):

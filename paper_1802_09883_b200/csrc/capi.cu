@@ -261,13 +261,15 @@ void *cache_get(size_t bytes) {
 }
 
 // Enqueue the whole GroupBy (deposit into a fresh slot table / partitions,
-// then fold + Eq. 1 into out, or merge into an accumulator).
+// then fold + Eq. 1 into out, or merge into an accumulator).  deposit_only:
+// stop after the deposit (paths 0 and 1 leave the absolute-level slot table
+// at the workspace's table offsets; the split form reads it from there).
 int enqueue_groupby(const int32_t *keys, const void *vals, int64_t n, int32_t G, int32_t K, int32_t dt,
                     void *out, int merge, int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *ws,
-                    size_t ws_bytes, cudaStream_t st, uint32_t **flags_out) {
+                    size_t ws_bytes, cudaStream_t st, uint32_t **flags_out, bool deposit_only = false) {
     const int path = choose_path(G, K, dt);
     t_path = path;
-    if (path < 0) return REPRO_EINVAL;
+    if (path < 0 || (deposit_only && path == 2)) return REPRO_EINVAL;
     if (ws_bytes < ws_bytes_for(path, n, G, K, dt)) return REPRO_ENOMEM;
     if (path == 0) {
         OnchipWs w = carve_onchip(ws, n, G, K, dt);
@@ -279,7 +281,7 @@ int enqueue_groupby(const int32_t *keys, const void *vals, int64_t n, int32_t G,
         int rc = timed(label, st, [&] {
             return launch_onchip_any(dt, K, keys, vals, n, G, w.kglob, w.slots, w.flags, st, &t_launches);
         });
-        if (rc) return map_launch(rc);
+        if (rc || deposit_only) return map_launch(rc);
         rc = timed("fold", st, [&] {
             return launch_fold(dt, K, G, w.kglob, w.slots, merge, acc_k, acc_C, acc_D, out, w.flags, st,
                                &t_launches);
@@ -290,8 +292,9 @@ int enqueue_groupby(const int32_t *keys, const void *vals, int64_t n, int32_t G,
     *flags_out = flags;
     if (cudaMemsetAsync(flags, 0, ALIGN, st) != cudaSuccess) return REPRO_ECUDA;
     if (path == 1)
-        return map_launch(launch_sweep(dt, K, keys, vals, n, G, (char *)ws + ALIGN, ws_bytes - ALIGN, merge, acc_k,
-                                       acc_C, acc_D, out, flags, st, &t_launches));
+        return map_launch(launch_sweep(dt, K, keys, vals, n, G, (char *)ws + ALIGN, ws_bytes - ALIGN, merge,
+                                       deposit_only ? nullptr : acc_k, acc_C, acc_D, deposit_only ? nullptr : out,
+                                       flags, st, &t_launches));
     int rc = launch_partitioned(dt, K, keys, vals, n, G, (char *)ws + ALIGN, ws_bytes - ALIGN, merge, acc_k,
                                 acc_C, acc_D, out, flags, st, &t_launches);
     return map_launch(rc);
@@ -416,6 +419,100 @@ int repro_groupby_sum(const int32_t *keys, const void *vals, int64_t n, int32_t 
         return rc;
     }
     return finish_blocking(flags, 0);
+}
+
+// ---- split form of the single-column GroupBy (multi-GPU exchange) ---------
+
+int repro_groupby_table(int64_t n, int32_t n_groups, int32_t fold, int32_t dtype, int64_t *offsets,
+                        int64_t *counts) {
+    if (n < 0 || !valid_shape(n_groups, fold, dtype) || !offsets || !counts) return REPRO_EINVAL;
+    const int path = choose_path(n_groups, fold, dtype);
+    if (path != 0 && path != 1) return REPRO_EINVAL;
+    OnchipWs w = carve_onchip(nullptr, n, n_groups, fold, dtype);  // path 1 uses the same leading layout
+    offsets[0] = (int64_t)(uintptr_t)w.flags;
+    offsets[1] = (int64_t)(uintptr_t)w.kglob;
+    offsets[2] = (int64_t)(uintptr_t)w.slots;
+    counts[0] = 1;
+    counts[1] = n_groups;
+    counts[2] = (int64_t)n_groups * slot_count(dtype, fold) * 2;
+    return REPRO_OK;
+}
+
+int repro_nvls_table_allreduce_async(void *mc_workspace, const int64_t *offsets, const int64_t *counts, int32_t rank,
+                                     int32_t world, void *stream) {
+    t_launches = 0;
+    if (!mc_workspace || !offsets || !counts || world < 1 || rank < 0 || rank >= world) return REPRO_EINVAL;
+    if (((uintptr_t)mc_workspace) % ALIGN || offsets[0] % 4 || offsets[1] % 4 || offsets[2] % 8 || counts[0] != 1)
+        return REPRO_EINVAL;
+    char *b = (char *)mc_workspace;
+    cudaStream_t st = (cudaStream_t)stream;
+    return map_launch(timed("nvls_reduce", st, [&] {
+        return launch_nvls_reduce((uint32_t *)(b + offsets[0]), (int32_t *)(b + offsets[1]), counts[1],
+                                  (unsigned long long *)(b + offsets[2]), counts[2], rank, world, st, &t_launches);
+    }));
+}
+
+int repro_groupby_deposit_async(const int32_t *keys, const void *vals, int64_t n, int32_t n_groups, int32_t fold,
+                                int32_t dtype, void *workspace, size_t ws_bytes, void *stream) {
+    t_launches = 0;
+    if (n < 0 || !valid_shape(n_groups, fold, dtype) || !workspace) return REPRO_EINVAL;
+    if (n > 0 && (!keys || !vals)) return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    uint32_t *flags = nullptr;
+    return enqueue_groupby(keys, vals, n, n_groups, fold, dtype, nullptr, 0, nullptr, nullptr, nullptr, workspace,
+                           ws_bytes, (cudaStream_t)stream, &flags, true);
+}
+
+int repro_groupby_finish_async(int64_t n, int32_t n_groups, int32_t fold, int32_t dtype, void *out, void *workspace,
+                               size_t ws_bytes, void *stream, int32_t *d_status) {
+    t_launches = 0;
+    if (n < 0 || !valid_shape(n_groups, fold, dtype) || !out || !workspace || !d_status) return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    const int path = choose_path(n_groups, fold, dtype);
+    if ((path != 0 && path != 1) || ws_bytes < ws_bytes_for(path, n, n_groups, fold, dtype)) return REPRO_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    OnchipWs w = carve_onchip(workspace, n, n_groups, fold, dtype);
+    int rc = timed("fold", st, [&] {
+        return launch_fold(dtype, fold, n_groups, w.kglob, w.slots, 0, nullptr, nullptr, nullptr, out, w.flags, st,
+                           &t_launches);
+    });
+    if (rc) return map_launch(rc);
+    return map_launch(timed("status", st, [&] { return launch_status(w.flags, d_status, st, &t_launches); }));
+}
+
+int repro_groupby_window_limbs_async(int64_t n, int32_t n_groups, int32_t fold, int32_t dtype,
+                                     const int32_t *k_global, int64_t *limbs, void *workspace, size_t ws_bytes,
+                                     void *stream) {
+    t_launches = 0;
+    if (n < 0 || !valid_shape(n_groups, fold, dtype) || !k_global || !limbs || !workspace) return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    const int path = choose_path(n_groups, fold, dtype);
+    if ((path != 0 && path != 1) || ws_bytes < ws_bytes_for(path, n, n_groups, fold, dtype)) return REPRO_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    OnchipWs w = carve_onchip(workspace, n, n_groups, fold, dtype);
+    return map_launch(timed("slot_limbs", st, [&] {
+        return launch_slot_limbs(dtype, fold, n_groups, k_global, w.slots, limbs, st, &t_launches);
+    }));
+}
+
+int repro_groupby_finish_limbs_async(int64_t n, int32_t n_groups, int32_t fold, int32_t dtype, int32_t g0,
+                                     int32_t count, const int32_t *k_range, const int64_t *limbs_range,
+                                     void *out_range, void *workspace, size_t ws_bytes, void *stream,
+                                     int32_t *d_status) {
+    t_launches = 0;
+    if (n < 0 || !valid_shape(n_groups, fold, dtype) || !workspace || !d_status) return REPRO_EINVAL;
+    if (g0 < 0 || count < 0 || (int64_t)g0 + count > n_groups) return REPRO_EINVAL;
+    if (count > 0 && (!k_range || !limbs_range || !out_range)) return REPRO_EINVAL;
+    if (((uintptr_t)workspace) % ALIGN) return REPRO_EINVAL;
+    const int path = choose_path(n_groups, fold, dtype);
+    if ((path != 0 && path != 1) || ws_bytes < ws_bytes_for(path, n, n_groups, fold, dtype)) return REPRO_EINVAL;
+    cudaStream_t st = (cudaStream_t)stream;
+    OnchipWs w = carve_onchip(workspace, n, n_groups, fold, dtype);
+    int rc = timed("limbs_finalize", st, [&] {
+        return launch_limbs_finalize(dtype, fold, count, k_range, limbs_range, out_range, w.flags, st, &t_launches);
+    });
+    if (rc) return map_launch(rc);
+    return map_launch(timed("status", st, [&] { return launch_status(w.flags, d_status, st, &t_launches); }));
 }
 
 // ---- multi-column GroupBy (several SUMs + COUNT in one pass) ---------------
@@ -1171,7 +1268,6 @@ static uint32_t *small_flags() {
 int repro_acc_merge(repro_acc *dst, const repro_acc *src) {
     t_launches = 0;
     if (!dst || !src || dst->G != src->G || dst->K != src->K || dst->dt != src->dt) return REPRO_EINVAL;
-    if (dst == src) return REPRO_EINVAL;
     std::lock_guard<std::mutex> lock(g_cache.mu);
     uint32_t *f = small_flags();
     if (!f) return REPRO_ENOMEM;

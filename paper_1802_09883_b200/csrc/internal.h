@@ -81,6 +81,13 @@ int launch_fold(int DT, int K, int32_t G, const int32_t *kglob, const unsigned l
                 int merge, int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *out,
                 uint32_t *status, cudaStream_t st, int *launches);
 
+// multi-GPU exchange of the slot table: K slot words under the global tops,
+// and the read-out of a group range from summed limbs
+int launch_slot_limbs(int DT, int K, int32_t G, const int32_t *kg, const unsigned long long *slots, int64_t *limbs,
+                      cudaStream_t st, int *launches);
+int launch_limbs_finalize(int DT, int K, int32_t count, const int32_t *kg, const int64_t *limbs, void *out,
+                          uint32_t *status, cudaStream_t st, int *launches);
+
 // canonical state -> Eq. 1 read-out
 int launch_finalize(int DT, int K, int32_t G, const int32_t *k, const int64_t *C, const int64_t *D,
                     void *out, uint32_t *status, cudaStream_t st, int *launches);
@@ -121,6 +128,10 @@ size_t sweep_workspace_bytes(int64_t n, int32_t G, int K, int DT);
 int launch_sweep(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G, void *ws,
                  size_t ws_bytes, int merge, int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *out,
                  uint32_t *status, cudaStream_t st, int *launches);
+
+// ---- NVLS (multimem) all-reduce of a slot table (k_nvls.cu) --------------
+int launch_nvls_reduce(uint32_t *mc_flags, int32_t *mc_kglob, int64_t nk, unsigned long long *mc_slots, int64_t ns,
+                       int rank, int world, cudaStream_t st, int *launches);
 
 // ---- non-reproducible baseline --------------------------------------------
 int launch_baseline(int DT, int variant, int acc64, const int32_t *keys, const void *vals,

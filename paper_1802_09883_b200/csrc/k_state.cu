@@ -150,8 +150,8 @@ k_import(int32_t G, const typename Fmt<DT>::V *__restrict__ state, int32_t *k, i
 
 template <int DT, int K>
 __global__ void __launch_bounds__(TPB_STATE)
-k_merge_state(int32_t G, int32_t *dk, int64_t *dC, int64_t *dD, const int32_t *__restrict__ sk,
-              const int64_t *__restrict__ sC, const int64_t *__restrict__ sD) {
+k_merge_state(int32_t G, int32_t *dk, int64_t *dC, int64_t *dD, const int32_t *sk, const int64_t *sC,
+              const int64_t *sD) {  // src may alias dst (dst += dst): each thread reads its group before writing
     const int g = blockIdx.x * TPB_STATE + threadIdx.x;
     if (g >= G) return;
     __int128 Ta[K], Tb[K];
@@ -204,6 +204,45 @@ k_window_import(int32_t count, const int32_t *__restrict__ kg, const int64_t *__
     k[g] = kg[g];
 }
 
+// Multi-GPU exchange of the absolute-level slot table: the
+// K slot words under each group's GLOBAL top (the realignment of the paper's
+// demotion, is just a choice of slots), as int64 pairs
+// [g][l][lo, hi] for an integer SUM across ranks.
+template <int DT, int K>
+__global__ void __launch_bounds__(TPB_STATE)
+k_slot_limbs(int32_t G, const int32_t *__restrict__ kg, const unsigned long long *__restrict__ slots,
+             int64_t *__restrict__ limbs) {
+    constexpr int NS = Fmt<DT>::KMAX + K;
+    const int g = blockIdx.x * TPB_STATE + threadIdx.x;
+    if (g >= G) return;
+    const int k = kg[g];
+#pragma unroll
+    for (int l = 0; l < K; ++l) {
+        const unsigned long long *p = slots + ((size_t)g * NS + (k - l + K - 1)) * 2;
+        limbs[((size_t)g * K + l) * 2] = (int64_t)p[0];
+        limbs[((size_t)g * K + l) * 2 + 1] = (int64_t)p[1];
+    }
+}
+
+// canonical state + Eq. 1 of `count` groups from summed limbs (kg, limbs and
+// out indexed from the range's first group)
+template <int DT, int K>
+__global__ void __launch_bounds__(TPB_STATE)
+k_limbs_finalize(int32_t count, const int32_t *__restrict__ kg, const int64_t *__restrict__ limbs,
+                 typename Fmt<DT>::V *out, uint32_t *status) {
+    const int g = blockIdx.x * TPB_STATE + threadIdx.x;
+    if (g >= count) return;
+    uint32_t flags = 0;
+    __int128 T[K];
+#pragma unroll
+    for (int l = 0; l < K; ++l)
+        T[l] = ((__int128)limbs[((size_t)g * K + l) * 2 + 1] << 32) + (__int128)(unsigned long long)limbs[((size_t)g * K + l) * 2];
+    int64_t Cc[K], Dc[K];
+    store_state<DT, K>(g, T, nullptr, nullptr, Cc, Dc);
+    out[g] = eq1_finalize<DT, K>(kg[g], Cc, Dc, flags);
+    publish_flags(flags, status);
+}
+
 __global__ void k_status(const uint32_t *flags, int32_t *d_status) {
     const uint32_t f = *flags;
     d_status[0] = (f & FLAG_EINVAL) ? -1 : (f & FLAG_EKEY) ? -2 : (f & FLAG_EDOM) ? -3 : (f & FLAG_ERANGE) ? -4 : 0;
@@ -233,6 +272,21 @@ inline unsigned blocks_for(int64_t n) { return (unsigned)((n + TPB_STATE - 1) / 
 #define LAUNCH_TAIL()                                   \
     ++*launches;                                        \
     return cudaGetLastError() == cudaSuccess ? 0 : -2
+
+int launch_slot_limbs(int DT, int K, int32_t G, const int32_t *kg, const unsigned long long *slots, int64_t *limbs,
+                      cudaStream_t st, int *launches) {
+    if (G == 0) return 0;
+    DISPATCH(DT, K, (k_slot_limbs<dt_, k_><<<blocks_for(G), TPB_STATE, 0, st>>>(G, kg, slots, limbs)));
+    LAUNCH_TAIL();
+}
+
+int launch_limbs_finalize(int DT, int K, int32_t count, const int32_t *kg, const int64_t *limbs, void *out,
+                          uint32_t *status, cudaStream_t st, int *launches) {
+    if (count == 0) return 0;
+    DISPATCH(DT, K, (k_limbs_finalize<dt_, k_><<<blocks_for(count), TPB_STATE, 0, st>>>(
+                        count, kg, limbs, (typename Fmt<dt_>::V *)out, status)));
+    LAUNCH_TAIL();
+}
 
 int launch_fold(int DT, int K, int32_t G, const int32_t *kglob, const unsigned long long *slots, int merge,
                 int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *out, uint32_t *status,

@@ -1,32 +1,36 @@
 // k_sweep.cu -- the high-cardinality GroupBy:
-// PartitionAndAggregate (Alg. 4) in two passes over the
-// rows, for group counts above the on-chip table's capacity.
+// PartitionAndAggregate (Alg. 4) for group counts above
+// the on-chip table's capacity, in at most two passes over the rows' bytes
+// plus one over the keys.
 //
 // Groups are split into P <= 256 partitions of Gp = 2^gbits consecutive keys
-// (Gp sized so one partition's table fits on chip, F = f^d with d = 1,
+// (Gp sized so that one partition's table fits on chip: F = f^d with d = 1,
 // PAPER.md:1054-1058).
-//   1. k_sw_sample   reads 8192 evenly spaced keys; a partition holding >= 1/8
-//                    of them is HOT (skew, e.g. Zipf's head).
-//   2. k_sweep       one pass over the rows, one persistent block per SM over
-//                    a contiguous row range: hot-partition rows are deposited
-//                    on chip right away (table_core.cuh, the heavy partition
-//                    never goes back to HBM); every other row is ranked within
-//                    its tile per partition, staged in shared memory in
-//                    partition order, and written out in whole UNITS (8 fp64 /
-//                    16 fp32 rows: full 32-byte sectors of keys and values)
-//                    into the block's current CHUNK of that partition (chunks
-//                    come from a global pool, one atomic per chunk).  Rows
-//                    short of a unit wait in shared memory for the next tile.
-//   3. k_sw_lists    chunk lists per partition and work items (<= CPI chunks).
-//   4. k_sweep_acc   persistent blocks pull work items and run the on-chip
-//                    table over the item's chunks (local keys).
-// Both tables publish into the absolute-level slot table (kglob, slots), which
+//   1. k_sw_sample  8192 evenly spaced keys; a partition holding >= 1/8 of
+//                   them is HOT (skew, e.g. Zipf's head).
+//   2. k_sweep_hot  (hot partition only) one pass over the rows: hot rows are
+//                   deposited on chip right away (table_core.cuh; the heavy
+//                   partition never goes back to HBM), the others are
+//                   compacted, coalesced per warp, into a contiguous buffer.
+//   3. k_sw_hist    per cold block: rows per partition (the keys only).
+//   4. k_sw_scan    per (partition, block): exclusive scan -> every block's
+//                   destination range in every partition; partitions start on
+//                   whole quads (the gap is padded); accumulate work items.
+//   5. k_sweep_cold per tile: rank rows by partition (shared atomics), stage
+//                   them in partition order, write each partition's run to
+//                   the block's running position in that partition.  Runs of
+//                   consecutive tiles abut, so their partial sectors are
+//                   completed in L2 before write-back.
+//   6. k_sweep_acc  persistent blocks pull work items (row ranges of one
+//                   partition) and run the on-chip table over them.
+// Both tables publish into the absolute-level slot table (kglob, slots) that
 // k_fold (k_state.cu) turns into canonical states and Eq. 1 read-outs.  Each
 // group lives in exactly one partition; the order of rows inside a partition
 // is irrelevant (the accumulator is associative).
 //
-// HBM traffic: the rows are read once; cold rows are written once and read
-// once more (12 B per binary64 row each way); hot rows are read once.
+// HBM traffic per binary64 row: no hot partition: keys 4 (hist) + 12 read +
+// 12 written (scatter) + 12 read (accumulate) = 40 B; with a hot partition
+// holding a share h of the rows: 12 + (1 - h) (12 + 4 + 24 + 12) B.
 #include "common.cuh"
 #include "internal.h"
 #include "onchip_core.cuh"
@@ -38,19 +42,20 @@ namespace repro {
 
 namespace {
 
-constexpr int SW_TPB = 512;
-constexpr int SW_NW = SW_TPB / 32;
-constexpr int SW_TILE = 4 * SW_TPB;    // rows per sweep tile (one quad per thread)
-constexpr int SW_PMAX = 256;           // partitions of one sweep
-constexpr int SW_CHR = SW_TILE + 256;  // rows per chunk (>= TILE + unit: a tile's units span <= 2 chunks)
+constexpr int SW_TPB = 512;            // accumulate blocks (one per SM: the table)
+constexpr int SW_HTPB = 512;           // hot-partition pass (one block per SM: the hot table)
+constexpr int SW_CTPB = 256;           // histogram / scatter blocks
+constexpr int SW_CTILE = 2048;         // rows per scatter tile (two quads per thread)
+constexpr int SW_CBPS = 3;             // histogram / scatter blocks per SM
+constexpr int SW_PMAX = 256;           // partitions of one sweep (<= SW_CTPB: one thread per partition)
 constexpr int SW_SAMPLE = 8192;
-constexpr int SW_CPI = 256;            // chunks per accumulate work item
+constexpr int64_t SW_IROWS = 1 << 19;  // rows per accumulate work item (whole quads)
 constexpr int SW_TABLE_MAX = 168 * 1024;
-// control words: [0] chunks allocated, [1] work items, [2] queue head, [3] hot partition
-constexpr int SW_CTRL = 8;
-
-template <int DT>
-constexpr int sw_unit() { return DT == 1 ? 8 : 16; }
+// control words: [0] work items, [1] queue head, [3] hot partition, [4] rows
+// in the compacted cold buffer, [5] heavy groups of the hot partition,
+// [8 .. 8 + TAB_HMAX) their local keys
+constexpr int SW_CTRL = 8 + TAB_HMAX;
+constexpr int32_t SW_PAD = -1;         // key of a padding row (partition starts on whole quads)
 
 template <int DT, int K>
 int sw_gbits() {  // largest power-of-two partition whose table fits SW_TABLE_MAX
@@ -70,8 +75,8 @@ int traced(const char *name, cudaStream_t st, int *launches, Fn &&fn) {
 }
 
 struct SwPlan {
-    int gbits, Gp, P, grid;
-    int64_t max_chunks, max_items;
+    int gbits, Gp, P, grid, cgrid;  // grid: hot pass blocks (1 per SM); cgrid: histogram / scatter blocks
+    int64_t rows_cap, max_items;    // partitioned buffer rows; work items
 };
 
 template <int DT, int K>
@@ -81,20 +86,16 @@ SwPlan sw_plan(int64_t n, int32_t G) {
     pl.Gp = 1 << pl.gbits;
     pl.P = (int)(((int64_t)G + pl.Gp - 1) >> pl.gbits);
     pl.grid = device_props().sms;
-    pl.max_chunks = (n + SW_CHR - 1) / SW_CHR + (int64_t)pl.grid * pl.P + 1;
-    pl.max_items = pl.P + pl.max_chunks / SW_CPI + 1;
+    pl.cgrid = SW_CBPS * device_props().sms;
+    pl.rows_cap = n + 4 * (int64_t)pl.P + 4;
+    pl.max_items = pl.P + (n + SW_IROWS - 1) / SW_IROWS + 1;
     return pl;
 }
 
-template <int DT, int K>
-size_t sw_smem(const SwPlan &pl) {
+template <int DT>
+size_t sw_smem_cold() {
     using V = typename Fmt<DT>::V;
-    constexpr int U = sw_unit<DT>();
-    size_t b = (TabGeom<DT, K>::bytes(pl.Gp) + 15) & ~(size_t)15;
-    b += (size_t)SW_TILE * (4 + sizeof(V));
-    b += (size_t)pl.P * U * (4 + sizeof(V));
-    b += (size_t)pl.P * (9 * 4 + 2 * 8);
-    return b;
+    return (size_t)SW_CTILE * (4 + sizeof(V) + 2) + (size_t)SW_PMAX * 3 * 8;
 }
 
 struct SwWs {
@@ -102,9 +103,13 @@ struct SwWs {
     unsigned long long *slots;
     int32_t *ctrl;
     size_t zero_bytes;  // kglob .. ctrl (one memset)
-    int32_t *ckeys;
-    void *cvals;
-    int32_t *chunk_part, *chunk_rows, *plist, *items;
+    int32_t *bkeys;     // compacted cold rows (hot partition present)
+    void *bvals;
+    int32_t *pkeys;     // partitioned rows (local keys; SW_PAD in the gaps)
+    void *pvals;
+    int64_t *cnt;       // [cgrid][P] rows per (block, partition), then destination bases
+    int64_t *pstart;    // [P + 1] first row of each partition
+    int64_t *items;     // [max_items][3] partition, first row, end row
     size_t bytes;
 };
 
@@ -123,14 +128,25 @@ SwWs sw_carve(void *ws, int64_t n, int32_t G, const SwPlan &pl) {
     w.slots = (unsigned long long *)take(16 * (size_t)G * NS);
     w.ctrl = (int32_t *)take(4 * SW_CTRL);
     w.zero_bytes = o;
-    w.ckeys = (int32_t *)take(4 * (size_t)pl.max_chunks * SW_CHR);
-    w.cvals = take(sizeof(V) * (size_t)pl.max_chunks * SW_CHR);
-    w.chunk_part = (int32_t *)take(4 * (size_t)pl.max_chunks);
-    w.chunk_rows = (int32_t *)take(4 * (size_t)pl.max_chunks);
-    w.plist = (int32_t *)take(4 * (size_t)pl.max_chunks);
-    w.items = (int32_t *)take(12 * (size_t)pl.max_items);
+    w.bkeys = (int32_t *)take(4 * (size_t)n + 16);
+    w.bvals = take(sizeof(V) * (size_t)n + 16);
+    w.pkeys = (int32_t *)take(4 * (size_t)pl.rows_cap);
+    w.pvals = take(sizeof(V) * (size_t)pl.rows_cap);
+    w.cnt = (int64_t *)take(8 * (size_t)pl.cgrid * pl.P);
+    w.pstart = (int64_t *)take(8 * ((size_t)pl.P + 1));
+    w.items = (int64_t *)take(24 * (size_t)pl.max_items);
     w.bytes = o;
     return w;
+}
+
+// row range of cold block b over the cold input (the original rows, or the
+// compacted buffer when a partition is hot); quad-aligned
+__device__ __forceinline__ void cold_range(const int32_t *ctrl, int64_t n, int b, int nb, int64_t &r0, int64_t &r1) {
+    const int64_t ne = ctrl[3] >= 0 ? (int64_t)ctrl[4] : n;
+    int64_t chunk = (ne + nb - 1) / nb;
+    chunk = (chunk + 3) & ~(int64_t)3;
+    r0 = min(ne, (int64_t)b * chunk);
+    r1 = min(ne, r0 + chunk);
 }
 
 // 1. hot partition from evenly spaced keys (performance only: any choice
@@ -138,9 +154,12 @@ SwWs sw_carve(void *ws, int64_t n, int32_t G, const SwPlan &pl) {
 __global__ void __launch_bounds__(1024) k_sw_sample(const int32_t *__restrict__ keys, int64_t n, int32_t G, int gbits,
                                                     int P, int32_t *ctrl) {
     __shared__ int cnt[SW_PMAX];
+    __shared__ int hh[1 << 13];  // sampled rows per local key of the hot partition (Gp <= 2^13)
     __shared__ unsigned long long best;
+    __shared__ int s_hot;
     const int tid = threadIdx.x;
     for (int i = tid; i < SW_PMAX; i += 1024) cnt[i] = 0;
+    for (int i = tid; i < (1 << gbits); i += 1024) hh[i] = 0;
     if (tid == 0) best = 0;
     __syncthreads();
     for (int i = tid; i < SW_SAMPLE; i += 1024) {
@@ -154,101 +173,226 @@ __global__ void __launch_bounds__(1024) k_sw_sample(const int32_t *__restrict__ 
     for (int p = tid; p < P; p += 1024)
         if (cnt[p] > 0) atomicMax(&best, ((unsigned long long)cnt[p] << 32) | (unsigned)(SW_PMAX - 1 - p));
     __syncthreads();
+    const int samples = (int)min((int64_t)SW_SAMPLE, n);
     if (tid == 0) {
         const int c = (int)(best >> 32);
-        const int samples = (int)min((int64_t)SW_SAMPLE, n);
-        ctrl[3] = (c > 0 && 8 * c >= samples) ? SW_PMAX - 1 - (int)(best & 0xFFFFFFFFu) : -1;
+        s_hot = (c > 0 && 8 * c >= samples) ? SW_PMAX - 1 - (int)(best & 0xFFFFFFFFu) : -1;
+        ctrl[3] = s_hot;
+        ctrl[5] = 0;
     }
+    __syncthreads();
+    const int hot = s_hot;
+    if (hot < 0) return;
+    // heavy groups of the hot partition: >= 1/512 of the sampled rows each
+    for (int i = tid; i < SW_SAMPLE; i += 1024) {
+        const int64_t r = n * i / SW_SAMPLE;
+        if (r < n) {
+            const int32_t k = keys[r];
+            if ((uint32_t)k < (uint32_t)G && (k >> gbits) == hot) atomicAdd(&hh[k & ((1 << gbits) - 1)], 1);
+        }
+    }
+    __syncthreads();
+    const int thr = max(4, samples / 512);
+    for (int i = tid; i < (1 << gbits); i += 1024)
+        if (hh[i] >= thr) {
+            const int slot = atomicAdd(&ctrl[5], 1);
+            if (slot < TAB_HMAX) ctrl[8 + slot] = i;
+        }
 }
 
-// 2. the sweep
+// 2. hot partition present: one pass that deposits the hot rows on chip right
+// away (the heavy partition never goes back to HBM) and compacts the other
+// rows, coalesced per warp, into a contiguous buffer for 3-5.  Exits at once
+// when there is no hot partition.
 template <int DT, int K>
-__global__ void __launch_bounds__(SW_TPB, 1)
-k_sweep(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals, int64_t n, int32_t G,
-        int gbits, int P, int64_t chunk, int32_t *__restrict__ ckeys, typename Fmt<DT>::V *__restrict__ cvals,
-        int32_t *__restrict__ chunk_part, int32_t *__restrict__ chunk_rows, int64_t max_chunks,
-        int32_t *__restrict__ ctrl, int32_t *__restrict__ kglob, unsigned long long *__restrict__ slots,
-        uint32_t *__restrict__ status) {
+__global__ void __launch_bounds__(SW_HTPB, 1)
+k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals, int64_t n, int32_t G,
+            int gbits, int64_t chunk, int32_t *__restrict__ bkeys, typename Fmt<DT>::V *__restrict__ bvals,
+            int32_t *__restrict__ ctrl, int32_t *__restrict__ kglob, unsigned long long *__restrict__ slots,
+            uint32_t *__restrict__ status) {
     using V = typename Fmt<DT>::V;
-    constexpr int U = sw_unit<DT>();
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_mm[TAB_MM];
-    __shared__ int s_wsum[SW_NW];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int Gp = 1 << gbits;
     const int hot = ctrl[3];
+    if (hot < 0) return;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int Gp = 1 << gbits;
     const int64_t row0 = (int64_t)blockIdx.x * chunk;
     const int64_t row1 = min(n, row0 + chunk);
     if (row0 >= row1) return;
-
-    // shared memory: hot table | tile stage | leftover stage | per-partition words
-    const size_t tb = (TabGeom<DT, K>::bytes(Gp) + 15) & ~(size_t)15;
-    int32_t *tkeys = reinterpret_cast<int32_t *>(smem + tb);
-    V *tvals = reinterpret_cast<V *>(tkeys + SW_TILE);
-    int32_t *lkeys = reinterpret_cast<int32_t *>(tvals + SW_TILE);
-    V *lvals = reinterpret_cast<V *>(lkeys + P * U);
-    int64_t *dst0 = reinterpret_cast<int64_t *>(lvals + P * U);
-    int64_t *dst1 = dst0 + P;
-    int32_t *tcnt = reinterpret_cast<int32_t *>(dst1 + P);
-    int32_t *left = tcnt + P;   // rows waiting in the leftover stage
-    int32_t *off = left + P;    // tile-stage offset of this tile's rows
-    int32_t *lcur = off + P;    // leftovers at the start of this tile
-    int32_t *tcur = lcur + P;   // this tile's rows
-    int32_t *full = tcur + P;   // whole units flushed this tile
-    int32_t *msplit = full + P; // units that go to the current chunk
-    int32_t *cur = msplit + P;  // the block's current chunk of each partition (-1: none)
-    int32_t *fill = cur + P;    // rows used in it
-
-    const int Gh = hot >= 0 ? min(Gp, G - hot * Gp) : 1;
-    Table<DT, K, SW_TPB> tab(smem, s_mm, Gh, hot >= 0 ? (int64_t)hot * Gp : 0, kglob, slots);
-    if (hot >= 0) tab.clear();
-    for (int p = tid; p < P; p += SW_TPB) {
-        tcnt[p] = 0;
-        left[p] = 0;
-        cur[p] = -1;
-        fill[p] = 0;
-    }
+    const int nh = min(ctrl[5], TAB_HMAX);
+    Table<DT, K, SW_HTPB, 0, true> tab(smem, s_mm, min(Gp, G - hot * Gp), (int64_t)hot * Gp, kglob, slots, nh);
+    tab.clear();
+    __syncthreads();
+    tab.set_heavy(ctrl + 8, nh);
     uint32_t flags = 0;
     __syncthreads();
-
-    auto alloc = [&](int p) -> int {
-        const int c = atomicAdd(&ctrl[0], 1);
-        if (c >= max_chunks) { flags |= FLAG_EINVAL; return -1; }  // sizing guarantees this never happens
-        chunk_part[c] = p;
-        return c;
-    };
-
-    // one tile: the quad of this thread (`in` bit u: row u exists)
-    auto tile = [&](const QuadT<DT> &q, uint32_t in) {
-        int pp[4], rk[4], lk[4];
-        uint32_t hin = 0;
-        QuadT<DT> hq = q;
+    auto step = [&](const QuadT<DT> &q, uint32_t in) {
+        uint32_t hin = 0, cin = 0;
         int hk[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int32_t k = kq(q.k, u);
-            pp[u] = -1;
             hk[u] = 0;
             if (!((in >> u) & 1u)) continue;
             if ((uint32_t)k >= (uint32_t)G) { flags |= FLAG_EKEY; continue; }
-            const int p = k >> gbits;
-            lk[u] = k & (Gp - 1);
-            if (p == hot) {
-                hin |= 1u << u;
-                hk[u] = lk[u];
-            } else {
-                pp[u] = p;
-                rk[u] = atomicAdd(&tcnt[p], 1);
+            if ((k >> gbits) == hot) { hin |= 1u << u; hk[u] = k & (Gp - 1); }
+            else cin |= 1u << u;
+        }
+        // compaction: the warp's cold rows go to one reserved run of the buffer
+        const int c = __popc(cin);
+        int pre = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, pre, o);
+            if (lane >= o) pre += y;
+        }
+        int base = 0;
+        if (lane == 31 && pre > 0) base = atomicAdd(&ctrl[4], pre);
+        base = __shfl_sync(0xffffffffu, base, 31) + pre - c;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if ((cin >> u) & 1u) {
+                bkeys[base] = kq(q.k, u);
+                bvals[base] = q.v(u);
+                ++base;
             }
+        QuadT<DT> hq = q;
+        hq.k = make_int4(hk[0], hk[1], hk[2], hk[3]);
+        tab.quad(hq, hin, flags);
+    };
+    const int64_t nq = (row1 - row0) >> 2;
+    const int64_t steps = (nq + SW_HTPB - 1) / SW_HTPB;
+    QuadT<DT> nxt;
+    if (tid < nq) load_quad<DT, true>(keys, vals, row0 + 4 * (int64_t)tid, nxt);
+    for (int64_t s = 0; s < steps; ++s) {
+        const QuadT<DT> q = nxt;
+        const int64_t qi = s * SW_HTPB + tid;
+        if (qi + SW_HTPB < nq) load_quad<DT, true>(keys, vals, row0 + 4 * (qi + SW_HTPB), nxt);
+        step(q, qi < nq ? 0xFu : 0u);
+    }
+    const int tail = (int)(row1 - row0 - 4 * nq);
+    if (tail > 0) {
+        QuadT<DT> t;
+        load_partial<DT>(keys, vals, row0 + 4 * nq, tid == 0 ? tail : 0, t);
+        step(t, tid == 0 ? (1u << tail) - 1u : 0u);
+    }
+    tab.finish();
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if (lane == 0 && flags) atomicOr(status, flags);
+}
+
+// 3. rows per (cold block, partition); key check on the original rows
+__global__ void __launch_bounds__(SW_CTPB)
+k_sw_hist(const int32_t *__restrict__ keys, const int32_t *__restrict__ bkeys, int64_t n, int32_t G, int gbits,
+          int P, const int32_t *__restrict__ ctrl, int64_t *__restrict__ cnt, uint32_t *__restrict__ status) {
+    __shared__ int h[SW_PMAX];
+    const int tid = threadIdx.x;
+    const bool compacted = ctrl[3] >= 0;
+    const int32_t *k = compacted ? bkeys : keys;
+    int64_t r0, r1;
+    cold_range(ctrl, n, blockIdx.x, gridDim.x, r0, r1);
+    for (int p = tid; p < SW_PMAX; p += SW_CTPB) h[p] = 0;
+    __syncthreads();
+    uint32_t bad = 0;
+    for (int64_t r = r0 + tid; r < r1; r += SW_CTPB) {
+        const int32_t key = __ldg(k + r);
+        if ((uint32_t)key < (uint32_t)G) atomicAdd(&h[key >> gbits], 1);
+        else bad = FLAG_EKEY;
+    }
+    __syncthreads();
+    for (int p = tid; p < P; p += SW_CTPB) cnt[(size_t)blockIdx.x * P + p] = h[p];
+    bad = __reduce_or_sync(0xffffffffu, bad);
+    if ((tid & 31) == 0 && bad) atomicOr(status, bad);
+}
+
+// 4. destination bases (in place of the counts), partition starts on whole
+// quads with the gaps padded, work items (single block)
+__global__ void __launch_bounds__(1024)
+k_sw_scan(int64_t *__restrict__ cnt, int nb, int P, int64_t *__restrict__ pstart, int32_t *__restrict__ pkeys,
+          int64_t *__restrict__ items, int32_t *__restrict__ ctrl) {
+    __shared__ int64_t tot[SW_PMAX], start[SW_PMAX + 1];
+    const int tid = threadIdx.x;
+    // rows per partition (a thread per partition sums over the blocks)
+    for (int p = tid; p < P; p += 1024) {
+        int64_t t = 0;
+        for (int b = 0; b < nb; ++b) t += cnt[(size_t)b * P + p];
+        tot[p] = t;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t a = 0, it = 0;
+        for (int p = 0; p < P; ++p) {
+            start[p] = a;
+            for (int64_t r = 0; r < tot[p]; r += SW_IROWS, ++it) {  // items of whole quads
+                items[3 * it] = p;
+                items[3 * it + 1] = a + r;
+                items[3 * it + 2] = a + min(tot[p], r + SW_IROWS);
+            }
+            a += (tot[p] + 3) & ~(int64_t)3;
         }
-        if (hot >= 0) {  // block-uniform
-            hq.k = make_int4(hk[0], hk[1], hk[2], hk[3]);
-            tab.quad(hq, hin, flags);
+        start[P] = a;
+        ctrl[0] = (int32_t)it;
+        ctrl[1] = 0;
+    }
+    __syncthreads();
+    for (int p = tid; p <= P; p += 1024) pstart[p] = start[p];
+    for (int p = tid; p < P; p += 1024) {
+        int64_t a = start[p];
+        for (int b = 0; b < nb; ++b) {
+            const int64_t c = cnt[(size_t)b * P + p];
+            cnt[(size_t)b * P + p] = a;
+            a += c;
         }
+        for (int64_t r = a; r < start[p + 1]; ++r) pkeys[r] = SW_PAD;  // < 4 padding rows
+    }
+}
+
+// 5. the scatter of the cold rows
+template <int DT>
+__global__ void __launch_bounds__(SW_CTPB, SW_CBPS)
+k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals, int64_t n,
+             const int32_t *__restrict__ bkeys, const typename Fmt<DT>::V *__restrict__ bvals, int32_t G, int gbits,
+             int P, const int64_t *__restrict__ base, int32_t *__restrict__ pkeys,
+             typename Fmt<DT>::V *__restrict__ pvals, const int32_t *__restrict__ ctrl) {
+    using V = typename Fmt<DT>::V;
+    constexpr int TPB = SW_CTPB, NW = TPB / 32, TILE = SW_CTILE, QPT = TILE / (4 * TPB);
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_wsum[NW];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int Gp = 1 << gbits;
+    if (ctrl[3] >= 0) { keys = bkeys; vals = bvals; }
+    int64_t row0, row1;
+    cold_range(ctrl, n, blockIdx.x, gridDim.x, row0, row1);
+    if (row0 >= row1) return;
+    // shared memory: tile stage keys | values | partitions | per-partition words
+    int32_t *tkeys = reinterpret_cast<int32_t *>(smem);
+    V *tvals = reinterpret_cast<V *>(tkeys + TILE);
+    int64_t *run = reinterpret_cast<int64_t *>(tvals + TILE);  // next destination row of each partition
+    int32_t *tcnt = reinterpret_cast<int32_t *>(run + SW_PMAX);
+    int32_t *off = tcnt + SW_PMAX;
+    uint16_t *tpart = reinterpret_cast<uint16_t *>(off + SW_PMAX);
+    for (int p = tid; p < P; p += TPB) {
+        run[p] = base[(size_t)blockIdx.x * P + p];
+        tcnt[p] = 0;
+    }
+    __syncthreads();
+
+    auto tile = [&](const QuadT<DT> (&q)[QPT], const uint32_t (&in)[QPT]) {
+        int pp[QPT][4], rk[QPT][4];
+#pragma unroll
+        for (int i = 0; i < QPT; ++i)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int32_t k = kq(q[i].k, u);
+                pp[i][u] = -1;
+                if (((in[i] >> u) & 1u) && (uint32_t)k < (uint32_t)G) {
+                    pp[i][u] = k >> gbits;
+                    rk[i][u] = atomicAdd(&tcnt[pp[i][u]], 1);
+                }
+            }
         __syncthreads();  // B1: ranks complete
-        // per partition: tile-stage offsets (block scan), units to flush,
-        // destination chunks
-        {
+        {  // per partition: tile-stage offset (block scan)
             const int p = tid;
             const int T = p < P ? tcnt[p] : 0;
             int incl = T;
@@ -259,209 +403,122 @@ k_sweep(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict_
             }
             if (lane == 31) s_wsum[warp] = incl;
             __syncthreads();
-            int base = 0;
-            for (int w = 0; w < warp; ++w) base += s_wsum[w];
-            if (p < P) {
-                tcnt[p] = 0;
-                off[p] = base + incl - T;
-                const int L = left[p], tot = L + T, f = tot / U;
-                lcur[p] = L;
-                tcur[p] = T;
-                full[p] = f;
-                left[p] = tot - f * U;
-                if (f > 0) {
-                    int c = cur[p], fl = fill[p];
-                    if (c < 0) { c = alloc(p); fl = 0; }
-                    const int m = min(f, (SW_CHR - fl) / U);
-                    dst0[p] = c < 0 ? -1 : (int64_t)c * SW_CHR + fl;
-                    fl += m * U;
-                    if (m < f) {
-                        if (c >= 0) chunk_rows[c] = fl;
-                        c = alloc(p);
-                        fl = (f - m) * U;
-                        dst1[p] = c < 0 ? -1 : (int64_t)c * SW_CHR;
-                    }
-                    msplit[p] = m;
-                    cur[p] = c;
-                    fill[p] = fl;
-                }
-            }
+            int b0 = 0;
+            for (int w = 0; w < warp; ++w) b0 += s_wsum[w];
+            if (p < P) off[p] = b0 + incl - T;
         }
         __syncthreads();  // B2
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (pp[u] < 0) continue;
-            const int s = off[pp[u]] + rk[u];
-            tkeys[s] = lk[u];
-            tvals[s] = q.v(u);
-        }
-        __syncthreads();  // B3: tile stage complete
-        // flush: one warp per partition, 32 / U units per warp instruction
-        for (int p = warp; p < P; p += SW_NW) {
-            const int f = full[p], L = lcur[p], tot = L + tcur[p], o = off[p];
-            if (f > 0) {
-                const int m = msplit[p];
-                const int64_t d0 = dst0[p], d1 = dst1[p];
-                for (int j0 = 0; j0 < f; j0 += 32 / U) {
-                    const int j = j0 + lane / U, t = lane % U;
-                    if (j < f) {
-                        const int s = j * U + t;
-                        const int32_t kk = s < L ? lkeys[p * U + s] : tkeys[o + s - L];
-                        const V vv = s < L ? lvals[p * U + s] : tvals[o + s - L];
-                        const int64_t d = j < m ? d0 + (int64_t)j * U : d1 + (int64_t)(j - m) * U;
-                        if (d >= 0) {
-                            ckeys[d + t] = kk;
-                            cvals[d + t] = vv;
-                        }
-                    }
-                }
-                __syncwarp();
+        for (int i = 0; i < QPT; ++i)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (pp[i][u] < 0) continue;
+                const int s = off[pp[i][u]] + rk[i][u];
+                tkeys[s] = kq(q[i].k, u) & (Gp - 1);
+                tvals[s] = q[i].v(u);
+                tpart[s] = (uint16_t)pp[i][u];
             }
-            // rows short of a unit wait in the leftover stage
-            for (int s = max(L, f * U) + lane; s < tot; s += 32) {
-                lkeys[p * U + s - f * U] = tkeys[o + s - L];
-                lvals[p * U + s - f * U] = tvals[o + s - L];
-            }
+        __syncthreads();  // B3: tile stage complete, in partition order
+        const int ns = off[P - 1] + tcnt[P - 1];
+        for (int s = tid; s < ns; s += TPB) {  // consecutive threads: consecutive rows of a run
+            const int p = tpart[s];
+            const int64_t d = run[p] + (s - off[p]);
+            pkeys[d] = tkeys[s];
+            pvals[d] = tvals[s];
         }
-        // (the next tile's rank atomics touch only tcnt; its stage writes
-        // come after its B2)
+        __syncthreads();  // B4: the stage is read
+        for (int p = tid; p < P; p += TPB) {
+            run[p] += tcnt[p];
+            tcnt[p] = 0;
+        }
+        // (the next tile's rank atomics come after this thread's reset of its
+        // partitions and before the next B1; other partitions are reset by
+        // their own threads before those threads reach B1)
+        __syncthreads();
     };
 
     const int64_t nq = (row1 - row0) >> 2;
-    const int64_t steps = (nq + SW_TPB - 1) / SW_TPB;
-    QuadT<DT> nxt;
-    if (tid < nq) load_quad<DT, true>(keys, vals, row0 + 4 * (int64_t)tid, nxt);
+    const int64_t steps = (nq + TPB * QPT - 1) / (TPB * QPT);
+    QuadT<DT> nxt[QPT];
+#pragma unroll
+    for (int i = 0; i < QPT; ++i)
+        if (i * TPB + tid < nq) load_quad<DT, true>(keys, vals, row0 + 4 * (int64_t)(i * TPB + tid), nxt[i]);
     for (int64_t s = 0; s < steps; ++s) {
-        const QuadT<DT> q = nxt;
-        const int64_t qi = s * SW_TPB + tid;
-        if (qi + SW_TPB < nq) load_quad<DT, true>(keys, vals, row0 + 4 * (qi + SW_TPB), nxt);
-        tile(q, qi < nq ? 0xFu : 0u);
+        QuadT<DT> q[QPT];
+        uint32_t in[QPT];
+        const int64_t q0 = s * TPB * QPT + tid;
+#pragma unroll
+        for (int i = 0; i < QPT; ++i) {
+            q[i] = nxt[i];
+            in[i] = q0 + (int64_t)i * TPB < nq ? 0xFu : 0u;
+            const int64_t qn = q0 + (int64_t)(QPT + i) * TPB;
+            if (qn < nq) load_quad<DT, true>(keys, vals, row0 + 4 * qn, nxt[i]);
+        }
+        tile(q, in);
     }
     const int tail = (int)(row1 - row0 - 4 * nq);
     if (tail > 0) {
-        QuadT<DT> t;
-        load_partial<DT>(keys, vals, row0 + 4 * nq, tid == 0 ? tail : 0, t);
-        tile(t, tid == 0 ? (1u << tail) - 1u : 0u);
-    }
-    __syncthreads();
-    // the last rows of every partition: one partial unit, padded to whole quads
-    for (int p = tid; p < P; p += SW_TPB) {
-        const int nl = left[p];
-        int c = cur[p], fl = fill[p];
-        if (nl > 0) {
-            const int padded = (nl + 3) & ~3;
-            if (c < 0 || fl + padded > SW_CHR) {
-                if (c >= 0) chunk_rows[c] = fl;
-                c = alloc(p);
-                fl = 0;
-            }
-            if (c >= 0) {
-                const int64_t d = (int64_t)c * SW_CHR + fl;
-                for (int i = 0; i < padded; ++i) {
-                    ckeys[d + i] = i < nl ? lkeys[p * U + i] : -1;
-                    cvals[d + i] = i < nl ? lvals[p * U + i] : V(0);
-                }
-                fl += padded;
-            }
+        QuadT<DT> q[QPT];
+        uint32_t in[QPT];
+#pragma unroll
+        for (int i = 0; i < QPT; ++i) {
+            load_partial<DT>(keys, vals, row0 + 4 * nq, (i == 0 && tid == 0) ? tail : 0, q[i]);
+            in[i] = (i == 0 && tid == 0) ? (1u << tail) - 1u : 0u;
         }
-        if (c >= 0) chunk_rows[c] = fl;
+        tile(q, in);
     }
-    if (hot >= 0) tab.finish();
-    flags = __reduce_or_sync(0xffffffffu, flags);
-    if (lane == 0 && flags) atomicOr(status, flags);
 }
 
-// 3. chunk lists per partition and work items (single block)
-__global__ void __launch_bounds__(1024) k_sw_lists(const int32_t *__restrict__ chunk_part, int P,
-                                                   int32_t *__restrict__ plist, int32_t *__restrict__ items,
-                                                   int32_t *ctrl) {
-    __shared__ int pc[SW_PMAX], ps[SW_PMAX + 1], pi[SW_PMAX + 1], cursor[SW_PMAX];
-    const int tid = threadIdx.x;
-    const int nch = ctrl[0];
-    for (int p = tid; p < SW_PMAX; p += 1024) { pc[p] = 0; cursor[p] = 0; }
-    __syncthreads();
-    for (int c = tid; c < nch; c += 1024) atomicAdd(&pc[chunk_part[c]], 1);
-    __syncthreads();
-    if (tid == 0) {
-        int a = 0, b = 0;
-        for (int p = 0; p < P; ++p) {
-            ps[p] = a;
-            pi[p] = b;
-            a += pc[p];
-            b += (pc[p] + SW_CPI - 1) / SW_CPI;
-        }
-        ps[P] = a;
-        pi[P] = b;
-        ctrl[1] = b;
-        ctrl[2] = 0;
-    }
-    __syncthreads();
-    for (int c = tid; c < nch; c += 1024) {
-        const int p = chunk_part[c];
-        plist[ps[p] + atomicAdd(&cursor[p], 1)] = c;
-    }
-    for (int p = tid; p < P; p += 1024)
-        for (int i = pi[p], c0 = ps[p]; i < pi[p + 1]; ++i, c0 += SW_CPI) {
-            items[3 * i] = p;
-            items[3 * i + 1] = c0;
-            items[3 * i + 2] = min(c0 + SW_CPI, ps[p + 1]);
-        }
-}
-
-// 4. per-partition accumulation over the chunks of each work item
+// 6. per-partition accumulation over the work items (row ranges of one
+// partition, starting on whole quads)
 template <int DT, int K>
 __global__ void __launch_bounds__(SW_TPB, 1)
-k_sweep_acc(const int32_t *__restrict__ ckeys, const typename Fmt<DT>::V *__restrict__ cvals,
-            const int32_t *__restrict__ plist, const int32_t *__restrict__ chunk_rows,
-            const int32_t *__restrict__ items, int32_t *ctrl, int32_t G, int gbits, int32_t *__restrict__ kglob,
+k_sweep_acc(const int32_t *__restrict__ pkeys, const typename Fmt<DT>::V *__restrict__ pvals,
+            const int64_t *__restrict__ items, int32_t *ctrl, int32_t G, int gbits, int32_t *__restrict__ kglob,
             unsigned long long *__restrict__ slots, uint32_t *__restrict__ status) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_mm[TAB_MM];
     __shared__ int s_item;
-    __shared__ int s_cid[SW_CPI], s_pre[SW_CPI + 1];
     const int tid = threadIdx.x;
     const int Gp = 1 << gbits;
     uint32_t flags = 0;
     for (;;) {
-        if (tid == 0) s_item = atomicAdd(&ctrl[2], 1);
+        if (tid == 0) s_item = atomicAdd(&ctrl[1], 1);
         __syncthreads();
         const int it = s_item;
-        if (it >= ctrl[1]) break;
-        const int p = items[3 * it], c0 = items[3 * it + 1], nc = items[3 * it + 2] - c0;
+        if (it >= ctrl[0]) break;
+        const int p = (int)items[3 * it];
+        const int64_t r0 = items[3 * it + 1], r1 = items[3 * it + 2];
         Table<DT, K, SW_TPB> tab(smem, s_mm, min(Gp, G - p * Gp), (int64_t)p * Gp, kglob, slots);
         tab.clear();
-        if (tid < nc) s_cid[tid] = plist[c0 + tid];
         __syncthreads();
-        if (tid == 0) {  // quad prefix over the item's chunks
-            int a = 0;
-            for (int i = 0; i < nc; ++i) {
-                s_pre[i] = a;
-                a += chunk_rows[s_cid[i]] >> 2;
+        const int64_t nq = (r1 - r0 + 3) >> 2;  // the last quad may hold padding rows
+        constexpr int QA = 2;  // quads per thread per step (the next step's are in flight)
+        const int64_t steps = (nq + SW_TPB * QA - 1) / (SW_TPB * QA);
+        QuadT<DT> nxt[QA];
+#pragma unroll
+        for (int i = 0; i < QA; ++i)
+            if (i * SW_TPB + tid < nq) load_quad<DT, true>(pkeys, pvals, r0 + 4 * (int64_t)(i * SW_TPB + tid), nxt[i]);
+        for (int64_t s = 0; s < steps; ++s) {
+            QuadT<DT> cur[QA];
+#pragma unroll
+            for (int i = 0; i < QA; ++i) cur[i] = nxt[i];
+            const int64_t q0 = s * SW_TPB * QA + tid;
+#pragma unroll
+            for (int i = 0; i < QA; ++i) {
+                const int64_t qn = q0 + (int64_t)(QA + i) * SW_TPB;
+                if (qn < nq) load_quad<DT, true>(pkeys, pvals, r0 + 4 * qn, nxt[i]);
             }
-            s_pre[nc] = a;
-        }
-        __syncthreads();
-        const int nq = s_pre[nc];
-        auto row_of = [&](int qi) -> int64_t {  // first row of quad qi in the chunk storage
-            int lo = 0, hi = nc - 1;
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (s_pre[mid] <= qi) lo = mid;
-                else hi = mid - 1;
+#pragma unroll
+            for (int i = 0; i < QA; ++i) {
+                const QuadT<DT> &q = cur[i];
+                const int64_t rq = r0 + 4 * (q0 + (int64_t)i * SW_TPB);  // first row of the quad
+                uint32_t in = 0;
+                if (q0 + i * SW_TPB < nq)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) in |= (rq + u < r1 && kq(q.k, u) >= 0) ? 1u << u : 0u;
+                tab.quad(q, in, flags);
             }
-            return (int64_t)s_cid[lo] * SW_CHR + 4 * (int64_t)(qi - s_pre[lo]);
-        };
-        const int steps = (nq + SW_TPB - 1) / SW_TPB;
-        QuadT<DT> nxt;
-        if (tid < nq) load_quad<DT, true>(ckeys, cvals, row_of(tid), nxt);
-        for (int s = 0; s < steps; ++s) {
-            const QuadT<DT> q = nxt;
-            const int qi = s * SW_TPB + tid;
-            if (qi + SW_TPB < nq) load_quad<DT, true>(ckeys, cvals, row_of(qi + SW_TPB), nxt);
-            uint32_t in = 0;
-            if (qi < nq) in = (q.k.x >= 0 ? 1u : 0u) | (q.k.y >= 0 ? 2u : 0u) | (q.k.z >= 0 ? 4u : 0u) |
-                              (q.k.w >= 0 ? 8u : 0u);
-            tab.quad(q, in, flags);
         }
         tab.finish();
     }
@@ -476,24 +533,23 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
     using V = typename Fmt<DT>::V;
     const SwPlan pl = sw_plan<DT, K>(n, G);
     if (pl.P > SW_PMAX) return -1;
-    const size_t sm_sweep = sw_smem<DT, K>(pl);
-    const size_t sm_acc = TabGeom<DT, K>::bytes(pl.Gp);
-    if (sm_sweep > (size_t)device_props().smem_optin - 1024) return -1;
+    const size_t sm_cold = sw_smem_cold<DT>();
+    const size_t sm_tab = TabGeom<DT, K>::bytes(pl.Gp);  // accumulate
+    const size_t sm_hot = TabGeom<DT, K>::bytes(pl.Gp, TAB_HMAX);  // hot pass (+ heavy-group lane copies)
+    if (sm_hot > (size_t)device_props().smem_optin - 1024) return -1;
     SwWs w = sw_carve<DT, K>(ws, n, G, pl);
     if (w.bytes > ws_bytes) return -1;
-    static thread_local size_t conf_s = 0, conf_a = 0;
-    if (conf_s < sm_sweep) {
-        if (cudaFuncSetAttribute(k_sweep<DT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_sweep) !=
-            cudaSuccess)
-            return -2;
-        conf_s = sm_sweep;
-    }
-    if (conf_a < sm_acc) {
-        if (cudaFuncSetAttribute(k_sweep_acc<DT, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_acc) !=
-            cudaSuccess)
-            return -2;
-        conf_a = sm_acc;
-    }
+    static thread_local size_t conf_h = 0, conf_c = 0, conf_a = 0;
+    auto conf = [](auto kern, size_t &have, size_t want) {
+        if (have >= want) return true;
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want) != cudaSuccess)
+            return false;
+        have = want;
+        return true;
+    };
+    if (!conf(k_sweep_hot<DT, K>, conf_h, sm_hot) || !conf(k_sweep_cold<DT>, conf_c, sm_cold) ||
+        !conf(k_sweep_acc<DT, K>, conf_a, sm_tab))
+        return -2;
     if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return -2;
     int rc = 0;
     if (n > 0) {
@@ -504,23 +560,32 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
         int64_t chunk = (n + pl.grid - 1) / pl.grid;
         chunk = (chunk + 3) & ~(int64_t)3;
         const int grid = (int)((n + chunk - 1) / chunk);
-        rc = traced("sweep", st, launches, [&] {
-            k_sweep<DT, K><<<grid, SW_TPB, sm_sweep, st>>>(keys, (const V *)vals, n, G, pl.gbits, pl.P, chunk,
-                                                          w.ckeys, (V *)w.cvals, w.chunk_part, w.chunk_rows,
-                                                          pl.max_chunks, w.ctrl, w.kglob, w.slots, status);
+        rc = traced("sweep_hot", st, launches, [&] {  // returns at once when no partition is hot
+            k_sweep_hot<DT, K><<<grid, SW_HTPB, sm_hot, st>>>(keys, (const V *)vals, n, G, pl.gbits, chunk, w.bkeys,
+                                                             (V *)w.bvals, w.ctrl, w.kglob, w.slots, status);
         });
         if (rc) return rc;
-        rc = traced("sweep_lists", st, launches, [&] {
-            k_sw_lists<<<1, 1024, 0, st>>>(w.chunk_part, pl.P, w.plist, w.items, w.ctrl);
+        rc = traced("sweep_hist", st, launches, [&] {
+            k_sw_hist<<<pl.cgrid, SW_CTPB, 0, st>>>(keys, w.bkeys, n, G, pl.gbits, pl.P, w.ctrl, w.cnt, status);
+        });
+        if (rc) return rc;
+        rc = traced("sweep_scan", st, launches, [&] {
+            k_sw_scan<<<1, 1024, 0, st>>>(w.cnt, pl.cgrid, pl.P, w.pstart, w.pkeys, w.items, w.ctrl);
+        });
+        if (rc) return rc;
+        rc = traced("sweep_scatter", st, launches, [&] {
+            k_sweep_cold<DT><<<pl.cgrid, SW_CTPB, sm_cold, st>>>(keys, (const V *)vals, n, w.bkeys,
+                                                                 (const V *)w.bvals, G, pl.gbits, pl.P, w.cnt,
+                                                                 w.pkeys, (V *)w.pvals, w.ctrl);
         });
         if (rc) return rc;
         rc = traced("sweep_accumulate", st, launches, [&] {
-            k_sweep_acc<DT, K><<<device_props().sms, SW_TPB, sm_acc, st>>>(
-                w.ckeys, (const V *)w.cvals, w.plist, w.chunk_rows, w.items, w.ctrl, G, pl.gbits, w.kglob, w.slots,
-                status);
+            k_sweep_acc<DT, K><<<device_props().sms, SW_TPB, sm_tab, st>>>(
+                w.pkeys, (const V *)w.pvals, w.items, w.ctrl, G, pl.gbits, w.kglob, w.slots, status);
         });
         if (rc) return rc;
     }
+    if (!out && !acc_k) return 0;  // deposit only (the split form: the caller reads the slot table)
     return launch_fold(DT, K, G, w.kglob, w.slots, merge, acc_k, acc_C, acc_D, out, status, st, launches);
 }
 

@@ -48,6 +48,9 @@ namespace {
 #ifndef TAB_QPT
 #define TAB_QPT 1  // quads (4 rows) per thread per step; the next step's are in flight
 #endif
+#ifndef TAB_L2PF
+#define TAB_L2PF 0  // (measured slower: 0.419 -> 0.461 ms at 3 steps) steps ahead whose rows lane 0 of each warp prefetches into L2 (0: off)
+#endif
 #ifndef TAB_MINB256
 #define TAB_MINB256 2  // resident 256-thread blocks per SM the register budget is sized for
 #endif
@@ -87,6 +90,20 @@ k_table(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict_
         for (int i = 0; i < QPT; ++i) {
             const int64_t qn = q0 + (int64_t)(QPT + i) * TPB;
             if (qn < nq) load_quad<DT, VEC>(keys, vals, row0 + 4 * qn, nxt[i]);
+        }
+        if (TAB_L2PF > 0 && VEC && (tid & 31) == 0) {
+            // deeper memory-level parallelism without registers: the warp's
+            // rows TAB_L2PF steps ahead (contiguous: 32 quads per quad slot)
+            // are pulled into L2 by bulk prefetches
+#pragma unroll
+            for (int i = 0; i < QPT; ++i) {
+                const int64_t qp = q0 + (int64_t)(TAB_L2PF * QPT + i) * TPB;
+                if (qp + 32 <= nq) {
+                    const int64_t r = row0 + 4 * qp;
+                    l2_prefetch(keys + r, 128 * 4);
+                    l2_prefetch(vals + r, 128 * sizeof(typename Fmt<DT>::V));
+                }
+            }
         }
 #pragma unroll
         for (int i = 0; i < QPT; ++i) tab.quad(cur[i], q0 + (int64_t)i * TPB < nq ? 0xFu : 0u, flags);

@@ -16,6 +16,7 @@ namespace repro {
 constexpr uint32_t TAB_DRAIN_BIAS = 0x20000000u;  // |old| >= 2^29  <=>  (old + 2^29) has bit 30 or 31
 constexpr uint32_t TAB_DRAIN_MASK = 0xC0000000u;
 constexpr int TAB_MM = 32;  // shared control words of a Table (>= KMAX + 3)
+constexpr int TAB_HMAX = 32;  // heavy groups with per-lane counter copies (HH tables)
 
 template <int DT>
 struct QuadT;
@@ -70,6 +71,11 @@ __device__ __forceinline__ void load_partial(const int32_t *__restrict__ keys,
     else q.a = make_float4(v[0], v[1], v[2], v[3]);
 }
 
+// bulk prefetch of `bytes` (multiple of 16, 16-byte aligned) into L2
+__device__ __forceinline__ void l2_prefetch(const void *p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" :: "l"(p), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ uint32_t atom_add_shared(uint32_t a, uint32_t v) {
     uint32_t old;
     asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(a), "r"(v) : "memory");
@@ -112,15 +118,21 @@ template <int DT, int K>
 struct TabGeom {
     static constexpr int LIMBS = Fmt<DT>::LIMBS;
     static constexpr int CW = K * LIMBS;
-    __host__ __device__ static int gq(int G) { return (G + 1 + 3) & ~3; }
-    __host__ __device__ static size_t bytes(int G) { return (size_t)gq(G) * (4 * CW + 12); }
+    __host__ __device__ static int gq(int G, int nh = 0) { return (G + 1 + 32 * nh + 3) & ~3; }
+    __host__ __device__ static size_t bytes(int G, int nh = 0) {
+        return (size_t)gq(G, nh) * (4 * CW + 12) + (nh ? (size_t)G + 4 * TAB_HMAX : 0);
+    }
 };
 
 // One block's table.  Every method is entered by all threads of the block
 // (slow_quad and finish contain barriers; fast_quad is barrier-free).
 // GQC > 0: the counter-row stride is the compile-time constant GQC (>= gq(G)),
 // so every atomic's counter offset is an immediate.
-template <int DT, int K, int TPB, int GQC = 0>
+// HH: up to TAB_HMAX HEAVY groups (skewed keys, e.g. Zipf's head) get one
+// counter copy per lane in streaming mode -- virtual group G + 1 + 32 h +
+// lane, always bank = lane -- because many lanes of a warp adding to one
+// shared word serialise.  The copies are summed when published.
+template <int DT, int K, int TPB, int GQC = 0, bool HH = false>
 struct Table {
     using F = Fmt<DT>;
     using V = typename F::V;
@@ -141,17 +153,22 @@ struct Table {
     uint32_t big;   // OR of (old + 2^29) over observed counters
     bool first;
     int par;  // parity of slow_quad calls (block-uniform)
+    int nh;           // heavy groups (HH)
+    int8_t *hmap;     // local group -> heavy index or -1 (HH, shared, G entries)
+    int32_t *hkey;    // heavy index -> local group (HH, shared, TAB_HMAX entries)
     Extractors<DT, K> ex;
 
     __device__ __forceinline__ Table(unsigned char *mem, int *mm, int G_, int64_t gbase_, int32_t *kglob_,
-                                     unsigned long long *slots_)
+                                     unsigned long long *slots_, int nh_ = 0)
         : s_mm(mm), G(G_), gbase(gbase_), kglob(kglob_), slots(slots_), kuni(-1), lim(0), big(0), first(true),
-          par(0), ex(0) {
-        gq = GQC > 0 ? GQC : Geo::gq(G);
+          par(0), nh(HH ? nh_ : 0), ex(0) {
+        gq = GQC > 0 ? GQC : Geo::gq(G, nh);
         cnt = reinterpret_cast<uint32_t *>(mem);
         ktop = reinterpret_cast<int32_t *>(cnt + (size_t)CW * gq);
         knext = ktop + gq;
         rlist = knext + gq;
+        hkey = rlist + gq;
+        hmap = reinterpret_cast<int8_t *>(hkey + TAB_HMAX);
         cbase = (uint32_t)__cvta_generic_to_shared(cnt);
         wstride = 4u * (uint32_t)gq;
     }
@@ -160,15 +177,29 @@ struct Table {
         for (int i = threadIdx.x; i < CW * gq; i += TPB) cnt[i] = 0;
         for (int i = threadIdx.x; i < gq; i += TPB) { ktop[i] = 0; knext[i] = 0; }
         for (int i = threadIdx.x; i < F::KMAX + 3; i += TPB) s_mm[i] = i == 2 ? G : 0;  // all G groups at top 0
+        if (HH && nh > 0)
+            for (int i = threadIdx.x; i < G; i += TPB) hmap[i] = -1;
         kuni = -1;
         par = 0;
         lim = 0;
         big = 0;
         first = true;
     }
-    __device__ __forceinline__ void drain(int g, int w, int kt) {
-        const uint32_t c = atom_exch_shared(cbase + 4u * (uint32_t)g + (uint32_t)w * wstride, 0u);
-        if (c) slot_add<DT, K>(slots, gbase + g, kt - w / LIMBS, counter_part<DT>(w, c));
+    // set the heavy groups (HH; after clear() and a barrier, before a barrier)
+    __device__ __forceinline__ void set_heavy(const int32_t *keys_local, int count) {
+        if (!HH) return;
+        for (int h = threadIdx.x; h < count && h < nh; h += TPB) {
+            hkey[h] = keys_local[h];
+            hmap[keys_local[h]] = (int8_t)h;
+        }
+    }
+    // real group of a (virtual) group of the counter table
+    __device__ __forceinline__ int real_group(int vg) const {
+        return (HH && vg > G) ? hkey[(vg - G - 1) >> 5] : vg;
+    }
+    __device__ __forceinline__ void drain(int vg, int w, int kt) {
+        const uint32_t c = atom_exch_shared(cbase + 4u * (uint32_t)vg + (uint32_t)w * wstride, 0u);
+        if (c) slot_add<DT, K>(slots, gbase + real_group(vg), kt - w / LIMBS, counter_part<DT>(w, c));
     }
     // publish all counters of group g at window kt (no concurrent deposits)
     __device__ __forceinline__ void publish_all(int g, int kt) {
@@ -217,6 +248,10 @@ struct Table {
             exc |= (iu && !ok) ? 1u << u : 0u;
             key[u] = ok ? k : G;  // sink group
             val[u] = ok ? v : V(0);
+            if (HH && nh > 0 && ok) {  // a heavy group's row goes to this lane's copy
+                const int hh = hmap[k];
+                if (hh >= 0) key[u] = G + 1 + 32 * hh + (int)(threadIdx.x & 31);
+            }
         }
         uint32_t lo[4][K], hi[4][K], a[4];
 #pragma unroll
@@ -265,7 +300,7 @@ struct Table {
         if (big & TAB_DRAIN_MASK) {  // rare: drain every counter of this batch that is past 2^29
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                if (key[u] >= G) continue;
+                if (key[u] == G) continue;  // the sink
 #pragma unroll
                 for (int w = 0; w < CW; ++w) {
                     const uint32_t c = ld_shared_u32(a[u] + (uint32_t)w * wstride);
@@ -357,6 +392,18 @@ struct Table {
         for (int g = threadIdx.x; g < G; g += TPB) {
             publish_all(g, ktop[g]);
             if (ktop[g] > 0) atomicMax(&kglob[gbase + g], ktop[g]);
+        }
+        if (HH && nh > 0 && kuni >= 0) {  // the lane copies hold digits under kuni
+            for (int i = threadIdx.x; i < nh * CW; i += TPB) {
+                const int h = i / CW, w = i - h * CW;
+                int64_t T = 0;
+                uint32_t *p = cnt + (size_t)w * gq + G + 1 + 32 * h;
+                for (int l = 0; l < 32; ++l) {
+                    T += counter_part<DT>(w, p[l]);
+                    p[l] = 0;
+                }
+                slot_add<DT, K>(slots, gbase + hkey[h], kuni - w / LIMBS, T);
+            }
         }
         __syncthreads();
     }

@@ -206,3 +206,121 @@ def test_two_rank_slot_table_exchange_equals_single_oracle():
         assert p.exitcode == 0
     assert res[0][0] == res[1][0] == 3  # status bits OR-ed
     assert res[0][1] == res[1][1] == ref.tobytes()
+
+
+# ---- stream-ordered split form of the single-column GroupBy ----------------
+
+class FakeR:
+    """Test double of the binding's split-form calls (groupby_deposit_async,
+    groupby_table_views, groupby_finish_async, groupby_window_limbs_async,
+    groupby_finish_limbs_async) over CPU tensors: the deposit is the oracle's
+    state of the rank's rows laid out as the absolute-level slot table; the
+    read-outs are the exact-rational closed form of Eq. 1.  The workspace is a
+    dict of the three table tensors."""
+    F64, F32 = O.F64, O.F32
+
+    @staticmethod
+    def make_ws(G, K, dt):
+        ns = NS[dt] + K
+        return {"flags": torch.zeros(1, dtype=torch.int32), "kglob": torch.zeros(G, dtype=torch.int32),
+                "slots": torch.zeros(G * ns * 2, dtype=torch.int64), "dt": dt}
+
+    @staticmethod
+    def groupby_deposit_async(keys, vals, G, K, ws, stream=None):
+        k, v = keys.numpy(), vals.numpy()
+        bad = (k < 0) | (k >= G)
+        ws["flags"][0] = 1 if bad.any() else 0  # EKEY bit; the rows with bad keys deposit nothing
+        acc = OracleAccumulator(k[~bad], v[~bad], G, K)
+        kg, slots = _slot_table(acc)
+        ws["kglob"].copy_(kg)
+        ws["slots"].copy_(slots)
+
+    @staticmethod
+    def groupby_table_views(ws, n, G, K, dt):
+        return ws["flags"], ws["kglob"], ws["slots"]
+
+    @staticmethod
+    def _read(ws, G, K, g):
+        ns = NS[ws["dt"]] + K
+        S = ws["slots"].numpy().reshape(G, ns, 2)
+        k = int(ws["kglob"][g])
+        return k, [(int(S[g, k - l + K - 1, 1]) << 32) + int(S[g, k - l + K - 1, 0]) for l in range(K)]
+
+    @staticmethod
+    def _status(ws):
+        f = int(ws["flags"][0])
+        return -2 if f & 1 else -3 if f & 2 else -4 if f & 4 else 0
+
+    @staticmethod
+    def groupby_finish_async(n, G, K, dt, out, ws, status, stream=None):
+        bits = 64 if dt == O.F64 else 32
+        for g in range(G):
+            k, T = FakeR._read(ws, G, K, g)
+            out[g] = X.finalize_closed_form(k, T, bits)
+        status[0] = FakeR._status(ws)
+
+    @staticmethod
+    def groupby_window_limbs_async(n, G, K, dt, kglob, limbs, ws, stream=None):
+        ns = NS[dt] + K
+        S = ws["slots"].numpy().reshape(G, ns, 2)
+        L = limbs[: G * K * 2].view(G, K, 2)
+        for g in range(G):
+            k = int(kglob[g])
+            for l in range(K):
+                L[g, l, 0] = int(S[g, k - l + K - 1, 0])
+                L[g, l, 1] = int(S[g, k - l + K - 1, 1])
+
+    @staticmethod
+    def groupby_finish_limbs_async(n, G, K, dt, g0, cnt, k_range, limbs_range, out_range, ws, status, stream=None):
+        bits = 64 if dt == O.F64 else 32
+        L = limbs_range.view(cnt, K, 2)
+        for i in range(cnt):
+            T = [(int(L[i, l, 1]) << 32) + int(L[i, l, 0]) for l in range(K)]
+            out_range[i] = X.finalize_closed_form(int(k_range[i]), T, bits)
+        status[0] = FakeR._status(ws)
+
+
+def _split_worker(rank, world, port, keys, vals, G, K, rs, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1802_09883_b200 import dist as rdist
+        r0, r1 = rdist.shard_rows(keys.size, world, rank)
+        dt = O.F64 if vals.dtype == np.float64 else O.F32
+        ws = FakeR.make_ws(G, K, dt)
+        out = torch.empty(G, dtype=torch.float64 if dt == O.F64 else torch.float32)
+        status = torch.zeros(1, dtype=torch.int32)
+        rdist.groupby_sum_dist(FakeR, torch.from_numpy(keys[r0:r1]), torch.from_numpy(vals[r0:r1]), G, K, out, ws,
+                               status, reduce_scatter=rs)
+        q.put((rank, int(status.item()), out.numpy().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dtype,K,G,world,rs,badkey", [
+    (np.float64, 3, 11, 2, False, False), (np.float64, 3, 11, 2, True, False), (np.float32, 2, 7, 3, True, False),
+    (np.float64, 2, 5, 3, False, False), (np.float64, 3, 9, 2, True, True)])
+def test_split_form_exchange_equals_single_oracle(dtype, K, G, world, rs, badkey):
+    rng = np.random.default_rng(31 + G)
+    n = 4000
+    keys = rng.integers(0, G, n, dtype=np.int32)
+    vals = (rng.uniform(-1, 1, n) * np.exp2(rng.integers(-40, 40, n))).astype(dtype)
+    vals[-3:] *= 2.0 ** 60 if dtype == np.float64 else 2.0 ** 20  # only the last rank sees the top windows
+    if badkey:
+        keys[5] = G + 2  # rank 0's rows only: every rank must report EKEY
+    rc, ref = O.groupby_sum(keys, vals, G, K)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, keys, vals, G, K, rs, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r: (s, b) for r, s, b in (q.get(timeout=120) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    if badkey:
+        assert rc == O.EKEY and all(res[r][0] == O.EKEY for r in range(world))
+    else:
+        assert rc == O.OK and all(res[r] == (0, ref.tobytes()) for r in range(world))
