@@ -139,6 +139,16 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+_FP_RATE = {}
+
+
+def fp_add_rate(R, dt):
+    """Measured adds/s of the value type's FP pipe (repro_measure_fp_add_rate), once per dtype."""
+    if dt not in _FP_RATE:
+        _FP_RATE[dt] = R.measure_fp_add_rate(dt)
+    return _FP_RATE[dt]
+
+
 def ncu_traffic(config):
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
@@ -383,7 +393,12 @@ def run_workload(R, torch, args, config, n, G, K, dts, world, rank, local, steps
     else:
         outs = [torch.empty(G, dtype=cols[0].dtype, device="cuda")]
         ws = R.make_workspace(n, G, K, dt)
-    acc = R.Accumulator(G, K, dt) if (world > 1 and not multi and not array) else None
+    nvls = None
+    if world > 1 and not multi and not array and G < 4096:  # NVSwitch multicast table all-reduce when available
+        nvls = rdist.NvlsWorkspace.create(ws.numel())
+        if nvls is not None:
+            ws = nvls.buf
+    acc = None
 
     def step():
         if array:
@@ -401,13 +416,10 @@ def run_workload(R, torch, args, config, n, G, K, dts, world, rank, local, steps
         if world == 1:
             R.groupby_sum_async(keys, cols[0], G, K, outs[0], ws, status, stream)
             return
-        acc.reset()
-        acc.deposit(keys, cols[0])
-        if G >= 4096:  # reduce-scatter by group range + all-gather of the results
-            rdist.reduce_scatter_finalize(acc, outs[0])
-        else:
-            rdist.allreduce_state(acc)
-            acc.finalize(outs[0])
+        # stream-ordered split form: deposit into the slot table, integer
+        # collectives on the same stream (OR/MAX/SUM; G >= 4096: reduce-scatter
+        # by group range + all-gather of the outputs), read-out -- no host sync
+        rdist.groupby_sum_dist(R, keys, cols[0], G, K, outs[0], ws, status, stream=stream, nvls=nvls)
 
     for _ in range(max(warmup, 3)):
         step()
@@ -462,6 +474,18 @@ def run_workload(R, torch, args, config, n, G, K, dts, world, rank, local, steps
                 "kernel_share_of_step": kms / ms_b if ms_b else None, "alg_bytes_per_launch": alg_bytes,
                 "alg_bytes_per_row": row_bytes, "peak_source": peak_src,
                 "traffic_note": "DRAM bytes per launch from ncu --set full: profiles/r2_*_ncu_full.txt"}
+    if roof is not None:
+        # FP side of the roofline: 3K - 2 correctly rounded
+        # adds per deposited value at the MEASURED add rate of this GPU
+        rate = fp_add_rate(R, dt)
+        fp_adds = n * ncol * (3 * K - 2)
+        t_hbm = alg_bytes / (peak * 1e9)
+        t_fp = fp_adds / rate
+        roof.update({"fp_add_rate_measured": rate, "fp_adds_per_launch": fp_adds, "hbm_time_ms": t_hbm * 1e3,
+                     "fp_time_ms": t_fp * 1e3, "fp_pipe_frac": t_fp / (roof["kernel_ms"] * 1e-3),
+                     "roofline_time_ms": max(t_hbm, t_fp) * 1e3})
+        if t_fp > t_hbm:
+            roof["bound"] = "alu"
     step_bytes = n * row_bytes + G * vsz * (5 if multi else 1)
     res = {
         "workload": WORKLOADS.get(config), "config": config, "rows_per_gpu": n, "n_groups": G, "fold": K,

@@ -431,6 +431,16 @@ int repro_baseline_atomic_sum(const int32_t *keys, const void *vals, int64_t n,
                               int32_t n_groups, int32_t dtype, int32_t variant,
                               int32_t accumulate_f64, void *out, void *stream);
 
+/* Measurement support, not part of the method: the FP side of the roofline of
+ * SURVEY.md 8(d) ("the deposit FLOPs at the vector FP64/FP32 peak").  Runs
+ * independent chains of correctly rounded adds (__dadd_rn / __fadd_rn) of the
+ * value type `dtype` on every SM and writes the measured adds per second of
+ * the whole GPU (best of three launches) to *adds_per_s (host pointer).  The
+ * digit cascade costs 3K - 2 adds per value (Alg. 1 lines 10-16,
+ * PAPER.md:666-672).  Blocking (synchronises `stream`); EINVAL for an unknown
+ * dtype or a null pointer, ECUDA on a CUDA error. */
+int repro_measure_fp_add_rate(int32_t dtype, double *adds_per_s, void *stream);
+
 /* ------------------------------------------------------------------------
  * Introspection for tests and the benchmark.
  * ---------------------------------------------------------------------- */

@@ -94,6 +94,7 @@ _sig("repro_acc_window_export", ctypes.c_int, _vp, _vp, _vp)
 _sig("repro_acc_window_import", ctypes.c_int, _vp, _vp, _vp)
 _sig("repro_acc_window_import_range", ctypes.c_int, _vp, _i32, _i32, _vp, _vp)
 _sig("repro_baseline_atomic_sum", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp)
+_sig("repro_measure_fp_add_rate", ctypes.c_int, _i32, ctypes.POINTER(ctypes.c_double), _vp)
 _sig("repro_last_launch_count", _i32)
 _sig("repro_last_path", _i32)
 _sig("repro_onchip_max_groups", _i32, _i32, _i32)
@@ -581,6 +582,14 @@ def baseline_atomic_sum(keys, vals, n_groups: int, variant: int = 0, accumulate_
                                         _stream_ptr(stream))
     _check(st, "repro_baseline_atomic_sum")
     return out
+
+
+def measure_fp_add_rate(dtype: int, stream=None) -> float:
+    """Measured correctly rounded adds per second of the value type's FP pipe
+    on this GPU (the FP side of the roofline; repro_measure_fp_add_rate)."""
+    r = ctypes.c_double(0.0)
+    _check(_lib.repro_measure_fp_add_rate(dtype, ctypes.byref(r), _stream_ptr(stream)), "repro_measure_fp_add_rate")
+    return r.value
 
 
 def last_launch_count() -> int:

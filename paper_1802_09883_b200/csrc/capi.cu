@@ -749,6 +749,11 @@ int repro_synth_generate(int32_t config, uint64_t seed, int64_t r0, int64_t n, i
     return rc == -1 ? REPRO_EINVAL : map_launch(rc);
 }
 
+int repro_measure_fp_add_rate(int32_t dtype, double *adds_per_s, void *stream) {
+    if ((dtype != 0 && dtype != 1) || !adds_per_s) return REPRO_EINVAL;
+    return map_launch(measure_fp_add_rate(dtype, adds_per_s, (cudaStream_t)stream));
+}
+
 int repro_groupby_sum_sparse(const int64_t *keys, const void *vals, int64_t n, int64_t max_groups, int32_t fold,
                              int32_t dtype, int64_t *out_keys, void *out_vals, int64_t *n_groups_out) {
     t_launches = 0;

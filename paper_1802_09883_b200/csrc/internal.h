@@ -19,6 +19,9 @@ const DeviceProps &device_props();
 // -(K-1) .. KMAX, slot = level + K - 1.
 inline int slot_count(int DT, int K) { return (DT == 1 ? 25 : 7) + K; }
 
+// measured add rate of the FP pipe of `DT` on this GPU (k_peak.cu)
+int measure_fp_add_rate(int DT, double *adds_per_s, cudaStream_t st);
+
 // ---- launchers (return 0 on success, -1 unsupported shape, -2 CUDA error) --
 int onchip_max_groups(int K, int DT);
 void set_onchip_variant(int v);
