@@ -51,6 +51,10 @@ WORKLOADS = {
     5: "f4 sum: 2^28 fp64 values +-(1+mant)2^e e in [-20,20] (config-1 values), keyless reproducible SUM, K=3",
     6: "f4 dot: 2^27 x 2 fp64 vectors +-(1+mant)2^e e in [-20,20], reproducible dot product, K=3",
 }
+# f1: arbitrary int64 keys -- an extra workload, not a BASELINE config
+SPARSE = dict(n=1 << 26, distinct=1 << 18)
+WORKLOADS[7] = ("f1 sparse keys: 2^26 rows, int64 keys = SplitMix64 of ids uniform over 2^18 (2^18 distinct "
+                "keys spread over int64), fp64 +-(1+mant)2^e e in [-20,20], K=3 (hash-mapped dense path)")
 # f4: keyless single-array SUM / dot -- extra workloads, not BASELINE configs
 ARRAY = {5: dict(n=1 << 28, dot=False), 6: dict(n=1 << 27, dot=True)}
 ORACLE_SAMPLE_ROWS = 1 << 27  # bounded oracle sample (cpu_baseline): <= 2^27 rows, well under 30 s of host work
@@ -360,6 +364,44 @@ def oracle_parity(R, torch, config, keys, cols, host, G, K, outs, counts):
             "rows_compared": int(hk.size)}
 
 
+def run_sparse(R, torch, steps, warmup):
+    """f1: repro_groupby_sum_sparse (hash table -> sorted dense ids -> dense
+    path; blocking) on host-generated int64 keys; parity against the oracle's
+    np.unique + O5 on the same rows."""
+    from inputs import synth
+    n, D, K = SPARSE["n"], SPARSE["distinct"], 3
+    seed = synth.SEED_BASE + 7
+    hk = synth.keys_sparse(seed, 0, n, D)
+    hv = synth.values_signed_mant_exp(synth.SEED_BASE + 1, 0, n)
+    keys, vals = torch.from_numpy(hk).cuda(), torch.from_numpy(hv).cuda()
+    for _ in range(max(3, warmup)):
+        uk, out = R.groupby_sum_sparse(keys, vals, D)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s = torch.cuda.current_stream()
+    e0.record(s)
+    for _ in range(steps):
+        uk, out = R.groupby_sum_sparse(keys, vals, D)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    peak, _ = peaks()
+    res = {"workload": WORKLOADS[7], "config": 7, "rows_per_gpu": n, "distinct_keys": int(uk.numel()), "fold": K,
+           "dtype": "f64", "ms_per_step": ms, "value": n / (ms * 1e-3), "unit": "rows/s",
+           "step_hbm_gbs": n * 16 / (ms * 1e-3) / 1e9, "step_roofline_frac": n * 16 / (ms * 1e-3) / 1e9 / peak,
+           "note": "blocking call (the distinct count is read back to size the dense pass); the step reads "
+                   "16 B/row of input (int64 key + fp64 value)"}
+    import oracle as O
+    t0 = time.perf_counter()
+    rc, ruk, rout = O.groupby_sum_sparse(hk, hv, K)
+    ok = rc == 0 and np.array_equal(uk.cpu().numpy(), ruk) and out.cpu().numpy().tobytes() == rout.tobytes()
+    res["parity"] = {"vs_oracle": "bit-exact" if ok else "MISMATCH", "groups": int(ruk.size), "rows_compared": n,
+                     "seconds": time.perf_counter() - t0}
+    del keys, vals
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_workload(R, torch, args, config, n, G, K, dts, world, rank, local, steps, warmup, *, parity=True,
                  atomic=True, headline=False):
     """Time the whole hot path on one workload; returns the result dict."""
@@ -604,6 +646,7 @@ def main():
                                        args.steps, args.warmup)
         subs["config4"] = run_workload(R, torch, args, 4, 1 << 30, 4, 3, "f64", world, rank, local,
                                        max(3, args.steps // 4), args.warmup)
+        subs["f1_sparse"] = run_sparse(R, torch, max(3, args.steps // 4), args.warmup)
         line["configs"] = subs
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -239,6 +239,14 @@ int repro_groupby_sum_sparse(const int64_t *keys, const void *vals, int64_t n,
                              int64_t *out_keys, void *out_vals,
                              int64_t *n_groups_out);
 
+/* The same over ARBITRARY int32 keys (every int32 value is a valid key;
+ * out_keys are the distinct keys ascending, sign-extended to int64).  keys:
+ * DEVICE int32[n].  Same outputs, errors and blocking as above. */
+int repro_groupby_sum_sparse_i32(const int32_t *keys, const void *vals, int64_t n,
+                                 int64_t max_groups, int32_t fold, int32_t dtype,
+                                 int64_t *out_keys, void *out_vals,
+                                 int64_t *n_groups_out);
+
 /* AVG / sample VARIANCE / STDDEV per group from reproducible SUMs (SURVEY.md
  * 8(f) f2; the paper reduces every float aggregate to SUM):
  * one fused pass computes SUM(x), SUM(x*x) and COUNT (proj 2 above), then,

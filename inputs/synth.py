@@ -103,6 +103,14 @@ def keys_zipf(seed: int, r0: int, r1: int, n_groups: int, s: float = 1.1, cdf=No
     return np.minimum(np.searchsorted(cdf, u, side="right"), n_groups - 1).astype(np.int32)
 
 
+def keys_sparse(seed: int, r0: int, r1: int, distinct: int) -> np.ndarray:
+    """Arbitrary int64 keys (the f1 workload): row id uniform in [0, distinct),
+    key = SplitMix64 of the id (column 7) shifted to 62 bits -- `distinct`
+    distinct keys spread over the int64 range, no order or density."""
+    ids = uniform_int(splitmix(seed, 0, _rows(r0, r1)), distinct)
+    return (splitmix(seed, 7, ids) >> np.uint64(2)).astype(np.int64)
+
+
 def generate(config: int, n: int | None = None, n_groups: int | None = None, r0: int = 0,
              seed: int | None = None):
     """(keys int32[n], vals) for BASELINE config `config` (rows r0 .. r0+n)."""

@@ -59,6 +59,7 @@ _sig("repro_groupby_sum_multi", ctypes.c_int, _vp, ctypes.POINTER(_vp), _i32, _i
      ctypes.POINTER(_vp), _vp)
 _sig("repro_groupby_multi_workspace_bytes", _sz, _i64, _i32, _i32, _i32, _i32, _i32)
 _sig("repro_groupby_sum_sparse", ctypes.c_int, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp, ctypes.POINTER(_i64))
+_sig("repro_groupby_sum_sparse_i32", ctypes.c_int, _vp, _vp, _i64, _i64, _i32, _i32, _vp, _vp, ctypes.POINTER(_i64))
 _sig("repro_groupby_moments", ctypes.c_int, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp)
 _sig("repro_groupby_multi_table", ctypes.c_int, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_i64),
      ctypes.POINTER(_i64))
@@ -357,8 +358,9 @@ def groupby_sum_multi(keys, cols, n_groups: int, fold: int = 3, proj: int = 0, o
 
 
 def groupby_sum_sparse(keys, vals, max_groups: int, fold: int = 3):
-    """Reproducible GroupBy-SUM over arbitrary int64 keys (repro_groupby_sum_sparse).
-    Returns (distinct keys ascending, their sums) as device tensors."""
+    """Reproducible GroupBy-SUM over arbitrary int64 or int32 keys
+    (repro_groupby_sum_sparse / _i32).  Returns (distinct keys ascending as
+    int64, their sums) as device tensors."""
     torch = _torch()
     dt = _dtype_code(vals)
     if keys.numel() != vals.numel():
@@ -366,9 +368,12 @@ def groupby_sum_sparse(keys, vals, max_groups: int, fold: int = 3):
     ok = torch.empty(max_groups, dtype=torch.int64, device=vals.device)
     ov = torch.empty(max_groups, dtype=vals.dtype, device=vals.device)
     d = _i64()
-    _check(_lib.repro_groupby_sum_sparse(_dev(keys, "keys", torch.int64), _dev(vals, "vals"), keys.numel(), max_groups,
-                                         fold, dt, _dev(ok, "out_keys", torch.int64), _dev(ov, "out_vals", vals.dtype),
-                                         ctypes.byref(d)), "repro_groupby_sum_sparse")
+    if keys.dtype == torch.int32:
+        fn, name, kdt = _lib.repro_groupby_sum_sparse_i32, "repro_groupby_sum_sparse_i32", torch.int32
+    else:
+        fn, name, kdt = _lib.repro_groupby_sum_sparse, "repro_groupby_sum_sparse", torch.int64
+    _check(fn(_dev(keys, "keys", kdt), _dev(vals, "vals"), keys.numel(), max_groups, fold, dt,
+              _dev(ok, "out_keys", torch.int64), _dev(ov, "out_vals", vals.dtype), ctypes.byref(d)), name)
     return ok[: d.value], ov[: d.value]
 
 

@@ -754,8 +754,12 @@ int repro_measure_fp_add_rate(int32_t dtype, double *adds_per_s, void *stream) {
     return map_launch(measure_fp_add_rate(dtype, adds_per_s, (cudaStream_t)stream));
 }
 
-int repro_groupby_sum_sparse(const int64_t *keys, const void *vals, int64_t n, int64_t max_groups, int32_t fold,
-                             int32_t dtype, int64_t *out_keys, void *out_vals, int64_t *n_groups_out) {
+}  // extern "C"
+
+namespace {
+template <typename KeyT>
+int groupby_sum_sparse_impl(const KeyT *keys, const void *vals, int64_t n, int64_t max_groups, int32_t fold,
+                            int32_t dtype, int64_t *out_keys, void *out_vals, int64_t *n_groups_out) {
     t_launches = 0;
     if (n < 0 || max_groups < 1 || max_groups > partition_max_groups(fold, dtype) || !valid_shape(1, fold, dtype) ||
         !out_keys || !out_vals || !n_groups_out)
@@ -791,6 +795,19 @@ int repro_groupby_sum_sparse(const int64_t *keys, const void *vals, int64_t n, i
         return rc;
     }
     return finish_blocking(flags, 0);
+}
+}  // namespace
+
+extern "C" {
+
+int repro_groupby_sum_sparse(const int64_t *keys, const void *vals, int64_t n, int64_t max_groups, int32_t fold,
+                             int32_t dtype, int64_t *out_keys, void *out_vals, int64_t *n_groups_out) {
+    return groupby_sum_sparse_impl(keys, vals, n, max_groups, fold, dtype, out_keys, out_vals, n_groups_out);
+}
+
+int repro_groupby_sum_sparse_i32(const int32_t *keys, const void *vals, int64_t n, int64_t max_groups, int32_t fold,
+                                 int32_t dtype, int64_t *out_keys, void *out_vals, int64_t *n_groups_out) {
+    return groupby_sum_sparse_impl(keys, vals, n, max_groups, fold, dtype, out_keys, out_vals, n_groups_out);
 }
 
 int repro_groupby_moments(const int32_t *keys, const void *vals, int64_t n, int32_t n_groups, int32_t fold,

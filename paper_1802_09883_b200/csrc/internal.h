@@ -67,10 +67,11 @@ int launch_square(int DT, const void *x, int64_t n, void *sq, cudaStream_t st, i
 int launch_moments(int DT, const void *s, const void *q, const int64_t *cnt, int32_t G, void *avg, void *var, void *sd,
                    cudaStream_t st, int *launches);
 
-// arbitrary int64 keys -> dense ids (k_sparse.cu)
+// arbitrary int64 / int32 keys -> dense ids (k_sparse.cu)
 uint64_t sparse_table_slots(int64_t max_groups);
 size_t sparse_scratch_bytes(int64_t n, int64_t max_groups);
-int sparse_map_keys(const int64_t *keys, int64_t n, int64_t max_groups, void *scratch, int64_t *sorted_out,
+template <typename KeyT>
+int sparse_map_keys(const KeyT *keys, int64_t n, int64_t max_groups, void *scratch, int64_t *sorted_out,
                     int32_t **ids_out, int64_t *d_out, uint32_t *status, cudaStream_t st, int *launches);
 
 // device copy of synth.py's seeded generator (bench/test support, k_synth.cu)

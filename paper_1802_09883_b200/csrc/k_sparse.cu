@@ -36,11 +36,17 @@ __device__ __forceinline__ uint64_t fmix64(uint64_t k) {
     return k;
 }
 
-__global__ void k_hash_insert(const int64_t *__restrict__ keys, int64_t n, unsigned long long *tk, uint64_t mask,
+// key -> table word: the key sign-extended to 64 bits with the top bit
+// flipped (0 = empty slot, so INT64_MIN is reserved; no int32 key maps to 0)
+template <typename KeyT>
+__device__ __forceinline__ unsigned long long key_word(KeyT k) { return (unsigned long long)(int64_t)k ^ FLIP; }
+
+template <typename KeyT>
+__global__ void k_hash_insert(const KeyT *__restrict__ keys, int64_t n, unsigned long long *tk, uint64_t mask,
                               uint32_t *status, unsigned long long *distinct) {
     uint32_t bad = 0;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long s = (unsigned long long)keys[i] ^ FLIP;
+        const unsigned long long s = key_word(keys[i]);
         if (s == 0ull) {
             bad = FLAG_EKEY;
             continue;
@@ -84,10 +90,11 @@ __global__ void k_hash_assign(const int64_t *__restrict__ sorted, int64_t d, con
         tid[find_slot(tk, mask, (unsigned long long)sorted[i] ^ FLIP)] = (int32_t)i;
 }
 
-__global__ void k_hash_map(const int64_t *__restrict__ keys, int64_t n, const unsigned long long *tk, uint64_t mask,
+template <typename KeyT>
+__global__ void k_hash_map(const KeyT *__restrict__ keys, int64_t n, const unsigned long long *tk, uint64_t mask,
                            const int32_t *__restrict__ tid, int32_t *ids) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const unsigned long long s = (unsigned long long)keys[i] ^ FLIP;
+        const unsigned long long s = key_word(keys[i]);
         ids[i] = s == 0ull ? -1 : tid[find_slot(tk, mask, s)];
     }
 }
@@ -125,7 +132,8 @@ size_t sparse_scratch_bytes(int64_t n, int64_t max_groups) {
 // number of distinct keys (the call synchronises `st` to read it).  Returns
 // 0, -1 when there are more than max_groups distinct keys (*d_out still set),
 // -2 on a CUDA error.
-int sparse_map_keys(const int64_t *keys, int64_t n, int64_t max_groups, void *scratch, int64_t *sorted_out,
+template <typename KeyT>
+int sparse_map_keys(const KeyT *keys, int64_t n, int64_t max_groups, void *scratch, int64_t *sorted_out,
                     int32_t **ids_out, int64_t *d_out, uint32_t *status, cudaStream_t st, int *launches) {
     const uint64_t cap = sparse_table_slots(max_groups), mask = cap - 1;
     const size_t mg = (size_t)std::max<int64_t>(max_groups, 1);
@@ -167,5 +175,10 @@ int sparse_map_keys(const int64_t *keys, int64_t n, int64_t max_groups, void *sc
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -2;
 }
+
+template int sparse_map_keys<int64_t>(const int64_t *, int64_t, int64_t, void *, int64_t *, int32_t **, int64_t *,
+                                      uint32_t *, cudaStream_t, int *);
+template int sparse_map_keys<int32_t>(const int32_t *, int64_t, int64_t, void *, int64_t *, int32_t **, int64_t *,
+                                      uint32_t *, cudaStream_t, int *);
 
 }  // namespace repro

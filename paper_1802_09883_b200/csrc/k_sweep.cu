@@ -44,13 +44,28 @@ namespace {
 
 constexpr int SW_TPB = 512;            // accumulate blocks (one per SM: the table)
 constexpr int SW_HTPB = 512;           // hot-partition pass (one block per SM: the hot table)
-constexpr int SW_CTPB = 256;           // histogram / scatter blocks
-constexpr int SW_CTILE = 2048;         // rows per scatter tile (two quads per thread)
-constexpr int SW_CBPS = 3;             // histogram / scatter blocks per SM
+#ifndef SW_STPB
+#define SW_STPB 256   // scatter block size
+#endif
+#ifndef SW_SQPT
+#define SW_SQPT 2     // quads per thread per scatter tile
+#endif
+#ifndef SW_CBPS64
+#define SW_CBPS64 2   // scatter blocks per SM, binary64 (shared memory: stage + carry)
+#endif
+#ifndef SW_CBPS32
+#define SW_CBPS32 3   // the same, binary32
+#endif
+constexpr int SW_CTPB = 256;           // histogram blocks
+constexpr int SW_CTILE = 4 * SW_SQPT * SW_STPB;  // rows per scatter tile
+constexpr int SW_RUN = 8;              // rows per written run unit: 32-byte sectors of keys and values
+// histogram / scatter blocks per SM (one histogram block per scatter block)
+template <int DT>
+constexpr int sw_cbps() { return DT == 1 ? SW_CBPS64 : SW_CBPS32; }
 constexpr int SW_PMAX = 256;           // partitions of one sweep (<= SW_CTPB: one thread per partition)
 constexpr int SW_SAMPLE = 8192;
 constexpr int64_t SW_IROWS = 1 << 19;  // rows per accumulate work item (whole quads)
-constexpr int SW_TABLE_MAX = 168 * 1024;
+constexpr int SW_TABLE_MAX = 200 * 1024;  // accumulate table (band layout, XB = 1)
 // control words: [0] work items, [1] queue head, [3] hot partition, [4] rows
 // in the compacted cold buffer, [5] heavy groups of the hot partition,
 // [8 .. 8 + TAB_HMAX) their local keys
@@ -60,7 +75,7 @@ constexpr int32_t SW_PAD = -1;         // key of a padding row (partition starts
 template <int DT, int K>
 int sw_gbits() {  // largest power-of-two partition whose table fits SW_TABLE_MAX
     int b = 13;
-    while (b > 8 && TabGeom<DT, K>::bytes(1 << b) > SW_TABLE_MAX) --b;
+    while (b > 8 && TabGeom<DT, K, 1>::bytes(1 << b) > SW_TABLE_MAX) --b;
     return b;
 }
 
@@ -86,24 +101,30 @@ SwPlan sw_plan(int64_t n, int32_t G) {
     pl.Gp = 1 << pl.gbits;
     pl.P = (int)(((int64_t)G + pl.Gp - 1) >> pl.gbits);
     pl.grid = device_props().sms;
-    pl.cgrid = SW_CBPS * device_props().sms;
-    pl.rows_cap = n + 4 * (int64_t)pl.P + 4;
-    pl.max_items = pl.P + (n + SW_IROWS - 1) / SW_IROWS + 1;
+    pl.cgrid = sw_cbps<DT>() * device_props().sms;
+    // every (scatter block, partition) range is padded to whole run units
+    pl.rows_cap = n + (int64_t)SW_RUN * pl.cgrid * pl.P + SW_RUN;
+    pl.max_items = pl.P + (pl.rows_cap + SW_IROWS - 1) / SW_IROWS + 1;
     return pl;
 }
 
+// scatter stage: the tile's rows + every partition's carried rows (< SW_RUN
+// each), in partition order
+constexpr int SW_STAGE = SW_CTILE + (SW_RUN - 1) * SW_PMAX;
 template <int DT>
 size_t sw_smem_cold() {
     using V = typename Fmt<DT>::V;
-    return (size_t)SW_CTILE * (4 + sizeof(V) + 2) + (size_t)SW_PMAX * 3 * 8;
+    return (size_t)SW_STAGE * (4 + sizeof(V) + 2) + (size_t)SW_PMAX * SW_RUN * (4 + sizeof(V)) +
+           (size_t)SW_PMAX * (8 + 6 * 4 + 8);
 }
 
 struct SwWs {
     int32_t *kglob;
     unsigned long long *slots;
     int32_t *ctrl;
-    size_t zero_bytes;  // kglob .. ctrl (one memset)
-    int32_t *bkeys;     // compacted cold rows (hot partition present)
+    int64_t *hcnt;      // [grid] cold rows each hot-pass block compacted
+    size_t zero_bytes;  // kglob .. hcnt (one memset)
+    int32_t *bkeys;     // compacted cold rows (hot partition present): block b's at [b chunk, b chunk + hcnt[b])
     void *bvals;
     int32_t *pkeys;     // partitioned rows (local keys; SW_PAD in the gaps)
     void *pvals;
@@ -127,6 +148,7 @@ SwWs sw_carve(void *ws, int64_t n, int32_t G, const SwPlan &pl) {
     w.kglob = (int32_t *)take(4 * (size_t)G);
     w.slots = (unsigned long long *)take(16 * (size_t)G * NS);
     w.ctrl = (int32_t *)take(4 * SW_CTRL);
+    w.hcnt = (int64_t *)take(8 * (size_t)pl.grid);
     w.zero_bytes = o;
     w.bkeys = (int32_t *)take(4 * (size_t)n + 16);
     w.bvals = take(sizeof(V) * (size_t)n + 16);
@@ -139,14 +161,34 @@ SwWs sw_carve(void *ws, int64_t n, int32_t G, const SwPlan &pl) {
     return w;
 }
 
-// row range of cold block b over the cold input (the original rows, or the
-// compacted buffer when a partition is hot); quad-aligned
-__device__ __forceinline__ void cold_range(const int32_t *ctrl, int64_t n, int b, int nb, int64_t &r0, int64_t &r1) {
-    const int64_t ne = ctrl[3] >= 0 ? (int64_t)ctrl[4] : n;
-    int64_t chunk = (ne + nb - 1) / nb;
+// where the hot pass left the compacted cold rows: hot block r's region
+// starts at r * hchunk (quad-aligned) and holds hcnt[r] rows
+struct ColdSrc {
+    const int64_t *hcnt;
+    int hgrid;
+    int64_t hchunk;
+};
+
+// row range of cold block b of nb over the cold input; quad-aligned.  No hot
+// partition: the original rows split evenly.  Hot partition: each hot-pass
+// region split into nb / hgrid parts (nb >= hgrid: cold grids are a multiple
+// of the SM count, hot grids at most the SM count).
+__device__ __forceinline__ void cold_range(const int32_t *ctrl, const ColdSrc &cs, int64_t n, int b, int nb,
+                                           int64_t &r0, int64_t &r1) {
+    int64_t lo = 0, ne = n;
+    int parts = nb, part = b;
+    if (ctrl[3] >= 0) {
+        parts = nb / cs.hgrid;
+        const int r = b / parts;
+        part = b - r * parts;
+        if (r >= cs.hgrid) { r0 = r1 = 0; return; }
+        lo = (int64_t)r * cs.hchunk;
+        ne = cs.hcnt[r];
+    }
+    int64_t chunk = (ne + parts - 1) / parts;
     chunk = (chunk + 3) & ~(int64_t)3;
-    r0 = min(ne, (int64_t)b * chunk);
-    r1 = min(ne, r0 + chunk);
+    r0 = lo + min(ne, (int64_t)part * chunk);
+    r1 = lo + min(ne, (int64_t)part * chunk + chunk);
 }
 
 // 1. hot partition from evenly spaced keys (performance only: any choice
@@ -208,11 +250,12 @@ template <int DT, int K>
 __global__ void __launch_bounds__(SW_HTPB, 1)
 k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals, int64_t n, int32_t G,
             int gbits, int64_t chunk, int32_t *__restrict__ bkeys, typename Fmt<DT>::V *__restrict__ bvals,
-            int32_t *__restrict__ ctrl, int32_t *__restrict__ kglob, unsigned long long *__restrict__ slots,
-            uint32_t *__restrict__ status) {
+            int32_t *__restrict__ ctrl, int64_t *__restrict__ hcnt, int32_t *__restrict__ kglob,
+            unsigned long long *__restrict__ slots, uint32_t *__restrict__ status) {
     using V = typename Fmt<DT>::V;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_mm[TAB_MM];
+    __shared__ int s_ccount;  // cold rows compacted by this block (its region starts at row0)
     const int hot = ctrl[3];
     if (hot < 0) return;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -221,8 +264,9 @@ k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restr
     const int64_t row1 = min(n, row0 + chunk);
     if (row0 >= row1) return;
     const int nh = min(ctrl[5], TAB_HMAX);
-    Table<DT, K, SW_HTPB, 0, true> tab(smem, s_mm, min(Gp, G - hot * Gp), (int64_t)hot * Gp, kglob, slots, nh);
+    Table<DT, K, SW_HTPB, 0, true, 1> tab(smem, s_mm, min(Gp, G - hot * Gp), (int64_t)hot * Gp, kglob, slots, nh);
     tab.clear();
+    if (tid == 0) s_ccount = 0;
     __syncthreads();
     tab.set_heavy(ctrl + 8, nh);
     uint32_t flags = 0;
@@ -239,7 +283,8 @@ k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restr
             if ((k >> gbits) == hot) { hin |= 1u << u; hk[u] = k & (Gp - 1); }
             else cin |= 1u << u;
         }
-        // compaction: the warp's cold rows go to one reserved run of the buffer
+        // compaction: the warp's cold rows go to one reserved run of the
+        // block's region (a shared counter: no global contention)
         const int c = __popc(cin);
         int pre = c;
 #pragma unroll
@@ -248,14 +293,14 @@ k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restr
             if (lane >= o) pre += y;
         }
         int base = 0;
-        if (lane == 31 && pre > 0) base = atomicAdd(&ctrl[4], pre);
-        base = __shfl_sync(0xffffffffu, base, 31) + pre - c;
+        if (lane == 31 && pre > 0) base = atomicAdd(&s_ccount, pre);
+        int64_t pos = row0 + __shfl_sync(0xffffffffu, base, 31) + pre - c;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if ((cin >> u) & 1u) {
-                bkeys[base] = kq(q.k, u);
-                bvals[base] = q.v(u);
-                ++base;
+                bkeys[pos] = kq(q.k, u);
+                bvals[pos] = q.v(u);
+                ++pos;
             }
         QuadT<DT> hq = q;
         hq.k = make_int4(hk[0], hk[1], hk[2], hk[3]);
@@ -264,11 +309,12 @@ k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restr
     const int64_t nq = (row1 - row0) >> 2;
     const int64_t steps = (nq + SW_HTPB - 1) / SW_HTPB;
     QuadT<DT> nxt;
-    if (tid < nq) load_quad<DT, true>(keys, vals, row0 + 4 * (int64_t)tid, nxt);
+    const bool vec = ((((uintptr_t)keys) | ((uintptr_t)vals)) & 15) == 0;  // (rows r0 are quad multiples)
+    if (tid < nq) load_quad_rt<DT>(keys, vals, row0 + 4 * (int64_t)tid, nxt, vec);
     for (int64_t s = 0; s < steps; ++s) {
         const QuadT<DT> q = nxt;
         const int64_t qi = s * SW_HTPB + tid;
-        if (qi + SW_HTPB < nq) load_quad<DT, true>(keys, vals, row0 + 4 * (qi + SW_HTPB), nxt);
+        if (qi + SW_HTPB < nq) load_quad_rt<DT>(keys, vals, row0 + 4 * (qi + SW_HTPB), nxt, vec);
         step(q, qi < nq ? 0xFu : 0u);
     }
     const int tail = (int)(row1 - row0 - 4 * nq);
@@ -277,104 +323,152 @@ k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restr
         load_partial<DT>(keys, vals, row0 + 4 * nq, tid == 0 ? tail : 0, t);
         step(t, tid == 0 ? (1u << tail) - 1u : 0u);
     }
-    tab.finish();
+    tab.finish();  // (barriers on both sides: every warp's compaction is done)
+    if (tid == 0) hcnt[blockIdx.x] = s_ccount;
     flags = __reduce_or_sync(0xffffffffu, flags);
     if (lane == 0 && flags) atomicOr(status, flags);
 }
 
-// 3. rows per (cold block, partition); key check on the original rows
+// 3. rows per (cold block, partition); key check on the original rows.
+// 16-byte key loads, four in flight per thread.
 __global__ void __launch_bounds__(SW_CTPB)
 k_sw_hist(const int32_t *__restrict__ keys, const int32_t *__restrict__ bkeys, int64_t n, int32_t G, int gbits,
-          int P, const int32_t *__restrict__ ctrl, int64_t *__restrict__ cnt, uint32_t *__restrict__ status) {
+          int P, const int32_t *__restrict__ ctrl, ColdSrc cs, int64_t *__restrict__ cnt,
+          uint32_t *__restrict__ status) {
     __shared__ int h[SW_PMAX];
     const int tid = threadIdx.x;
     const bool compacted = ctrl[3] >= 0;
     const int32_t *k = compacted ? bkeys : keys;
     int64_t r0, r1;
-    cold_range(ctrl, n, blockIdx.x, gridDim.x, r0, r1);
+    cold_range(ctrl, cs, n, blockIdx.x, gridDim.x, r0, r1);
     for (int p = tid; p < SW_PMAX; p += SW_CTPB) h[p] = 0;
     __syncthreads();
     uint32_t bad = 0;
-    for (int64_t r = r0 + tid; r < r1; r += SW_CTPB) {
-        const int32_t key = __ldg(k + r);
+    auto one = [&](int32_t key) {
         if ((uint32_t)key < (uint32_t)G) atomicAdd(&h[key >> gbits], 1);
         else bad = FLAG_EKEY;
+    };
+    int64_t r = r0;
+    if ((((uintptr_t)(k + r0)) & 15) == 0) {  // r0 is a multiple of 4; keys may be unaligned
+        constexpr int U = 4;
+        const int64_t nq = (r1 - r0) >> 2;
+        const int4 *kq4 = reinterpret_cast<const int4 *>(k + r0);
+        int64_t q = tid;
+        for (; q + (U - 1) * SW_CTPB < nq; q += U * SW_CTPB) {
+            int4 a[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) a[u] = __ldcs(kq4 + q + u * SW_CTPB);
+#pragma unroll
+            for (int u = 0; u < U; ++u) { one(a[u].x); one(a[u].y); one(a[u].z); one(a[u].w); }
+        }
+        for (; q < nq; q += SW_CTPB) {
+            const int4 a = __ldcs(kq4 + q);
+            one(a.x); one(a.y); one(a.z); one(a.w);
+        }
+        r = r0 + 4 * nq;
     }
+    for (r += tid; r < r1; r += SW_CTPB) one(__ldg(k + r));
     __syncthreads();
     for (int p = tid; p < P; p += SW_CTPB) cnt[(size_t)blockIdx.x * P + p] = h[p];
     bad = __reduce_or_sync(0xffffffffu, bad);
     if ((tid & 31) == 0 && bad) atomicOr(status, bad);
 }
 
-// 4. destination bases (in place of the counts), partition starts on whole
-// quads with the gaps padded, work items (single block)
+// 4. destination bases (in place of the counts): every (block, partition)
+// range is padded to whole run units of SW_RUN rows, so partitions and block
+// ranges start on 32-byte sectors of both columns; work items (single block)
+__device__ __forceinline__ int64_t sw_pad(int64_t c) { return (c + SW_RUN - 1) & ~(int64_t)(SW_RUN - 1); }
+
 __global__ void __launch_bounds__(1024)
 k_sw_scan(int64_t *__restrict__ cnt, int nb, int P, int64_t *__restrict__ pstart, int32_t *__restrict__ pkeys,
           int64_t *__restrict__ items, int32_t *__restrict__ ctrl) {
-    __shared__ int64_t tot[SW_PMAX], start[SW_PMAX + 1];
+    __shared__ int64_t part[4][SW_PMAX];
+    __shared__ int64_t start[SW_PMAX + 1];
     const int tid = threadIdx.x;
-    // rows per partition (a thread per partition sums over the blocks)
-    for (int p = tid; p < P; p += 1024) {
+    const int p = tid & (SW_PMAX - 1), quarter = tid >> 8;  // 4 threads per partition
+    const int b0 = nb * quarter / 4, b1 = nb * (quarter + 1) / 4;
+    if (p < P) {
         int64_t t = 0;
-        for (int b = 0; b < nb; ++b) t += cnt[(size_t)b * P + p];
-        tot[p] = t;
+#pragma unroll 8
+        for (int b = b0; b < b1; ++b) t += sw_pad(cnt[(size_t)b * P + p]);
+        part[quarter][p] = t;
     }
     __syncthreads();
     if (tid == 0) {
         int64_t a = 0, it = 0;
-        for (int p = 0; p < P; ++p) {
-            start[p] = a;
-            for (int64_t r = 0; r < tot[p]; r += SW_IROWS, ++it) {  // items of whole quads
-                items[3 * it] = p;
+        for (int q = 0; q < P; ++q) {
+            const int64_t tot = part[0][q] + part[1][q] + part[2][q] + part[3][q];
+            start[q] = a;
+            for (int64_t r = 0; r < tot; r += SW_IROWS, ++it) {  // items of whole run units
+                items[3 * it] = q;
                 items[3 * it + 1] = a + r;
-                items[3 * it + 2] = a + min(tot[p], r + SW_IROWS);
+                items[3 * it + 2] = a + min(tot, r + SW_IROWS);
             }
-            a += (tot[p] + 3) & ~(int64_t)3;
+            a += tot;
         }
         start[P] = a;
         ctrl[0] = (int32_t)it;
         ctrl[1] = 0;
     }
     __syncthreads();
-    for (int p = tid; p <= P; p += 1024) pstart[p] = start[p];
-    for (int p = tid; p < P; p += 1024) {
+    for (int q = tid; q <= P; q += 1024) pstart[q] = start[q];
+    if (p < P) {
         int64_t a = start[p];
-        for (int b = 0; b < nb; ++b) {
+        for (int w = 0; w < quarter; ++w) a += part[w][p];
+#pragma unroll 8
+        for (int b = b0; b < b1; ++b) {
             const int64_t c = cnt[(size_t)b * P + p];
             cnt[(size_t)b * P + p] = a;
-            a += c;
+            a += sw_pad(c);
         }
-        for (int64_t r = a; r < start[p + 1]; ++r) pkeys[r] = SW_PAD;  // < 4 padding rows
     }
 }
 
-// 5. the scatter of the cold rows
+// 5. the scatter of the cold rows.  Per tile: rank the rows by partition
+// (shared atomics), stage them in partition order behind the rows each
+// partition carried over from the previous tile, and write every
+// partition's whole run units (SW_RUN rows: full 32-byte sectors of keys and
+// of values) to the block's running position in that partition; the < SW_RUN
+// rows left over are carried to the next tile.  The block's last units are
+// padded with SW_PAD rows.  Every write is a whole, aligned sector, so DRAM
+// never has to merge partial sectors.
 template <int DT>
-__global__ void __launch_bounds__(SW_CTPB, SW_CBPS)
+__global__ void __launch_bounds__(SW_STPB, sw_cbps<DT>())
 k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals, int64_t n,
              const int32_t *__restrict__ bkeys, const typename Fmt<DT>::V *__restrict__ bvals, int32_t G, int gbits,
              int P, const int64_t *__restrict__ base, int32_t *__restrict__ pkeys,
-             typename Fmt<DT>::V *__restrict__ pvals, const int32_t *__restrict__ ctrl) {
+             typename Fmt<DT>::V *__restrict__ pvals, const int32_t *__restrict__ ctrl, ColdSrc cs) {
     using V = typename Fmt<DT>::V;
-    constexpr int TPB = SW_CTPB, NW = TPB / 32, TILE = SW_CTILE, QPT = TILE / (4 * TPB);
+    constexpr int TPB = SW_STPB, NW = TPB / 32, TILE = SW_CTILE, QPT = TILE / (4 * TPB);
+    static_assert(TPB >= SW_PMAX, "one thread per partition");
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_wsum[NW];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int Gp = 1 << gbits;
     if (ctrl[3] >= 0) { keys = bkeys; vals = bvals; }
     int64_t row0, row1;
-    cold_range(ctrl, n, blockIdx.x, gridDim.x, row0, row1);
+    cold_range(ctrl, cs, n, blockIdx.x, gridDim.x, row0, row1);
     if (row0 >= row1) return;
-    // shared memory: tile stage keys | values | partitions | per-partition words
-    int32_t *tkeys = reinterpret_cast<int32_t *>(smem);
-    V *tvals = reinterpret_cast<V *>(tkeys + TILE);
-    int64_t *run = reinterpret_cast<int64_t *>(tvals + TILE);  // next destination row of each partition
-    int32_t *tcnt = reinterpret_cast<int32_t *>(run + SW_PMAX);
+    // shared memory: stage values | carried values | run | stage keys |
+    // carried keys | counts | offsets | carried counts | flushed counts |
+    // new-row offsets | stage partitions
+    V *tvals = reinterpret_cast<V *>(smem);
+    V *cvals = tvals + SW_STAGE;
+    int64_t *run = reinterpret_cast<int64_t *>(cvals + SW_PMAX * SW_RUN);  // next destination row per partition
+    int32_t *tkeys = reinterpret_cast<int32_t *>(run + SW_PMAX);
+    int32_t *ckeys = tkeys + SW_STAGE;
+    int32_t *tcnt = ckeys + SW_PMAX * SW_RUN;
     int32_t *off = tcnt + SW_PMAX;
-    uint16_t *tpart = reinterpret_cast<uint16_t *>(off + SW_PMAX);
+    int32_t *ccnt = off + SW_PMAX;
+    int32_t *fl = ccnt + SW_PMAX;
+    int32_t *nb_ = fl + SW_PMAX;
+    int32_t *lim = nb_ + SW_PMAX;
+    int64_t *dbase = reinterpret_cast<int64_t *>(lim + SW_PMAX);  // (8-byte aligned: 7 int32 arrays of 256 after 8-byte data)
+    uint16_t *tpart = reinterpret_cast<uint16_t *>(dbase + SW_PMAX);
     for (int p = tid; p < P; p += TPB) {
         run[p] = base[(size_t)blockIdx.x * P + p];
         tcnt[p] = 0;
+        ccnt[p] = 0;
     }
     __syncthreads();
 
@@ -392,9 +486,9 @@ k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__rest
                 }
             }
         __syncthreads();  // B1: ranks complete
-        {  // per partition: tile-stage offset (block scan)
+        {  // per partition (thread p): carried + new rows -> stage offset, whole units to write
             const int p = tid;
-            const int T = p < P ? tcnt[p] : 0;
+            const int T = p < P ? ccnt[p] + tcnt[p] : 0;
             int incl = T;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -405,44 +499,66 @@ k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__rest
             __syncthreads();
             int b0 = 0;
             for (int w = 0; w < warp; ++w) b0 += s_wsum[w];
-            if (p < P) off[p] = b0 + incl - T;
+            if (p < P) {
+                const int o = b0 + incl - T;
+                off[p] = o;
+                nb_[p] = o + ccnt[p];  // the tile's new rows follow the carried ones
+                fl[p] = T & ~(SW_RUN - 1);
+                lim[p] = o + (T & ~(SW_RUN - 1));  // stage rows below lim[p] are written
+                dbase[p] = run[p] - o;             // destination of stage row s: dbase[p] + s
+            }
         }
         __syncthreads();  // B2
+        for (int i = tid; i < P * SW_RUN; i += TPB) {  // carried rows first
+            const int p = i / SW_RUN, j = i % SW_RUN;
+            if (j < ccnt[p]) {
+                const int s_ = off[p] + j;
+                tkeys[s_] = ckeys[i];
+                tvals[s_] = cvals[i];
+                tpart[s_] = (uint16_t)p;
+            }
+        }
 #pragma unroll
         for (int i = 0; i < QPT; ++i)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (pp[i][u] < 0) continue;
-                const int s = off[pp[i][u]] + rk[i][u];
-                tkeys[s] = kq(q[i].k, u) & (Gp - 1);
-                tvals[s] = q[i].v(u);
-                tpart[s] = (uint16_t)pp[i][u];
+                const int s_ = nb_[pp[i][u]] + rk[i][u];
+                tkeys[s_] = kq(q[i].k, u) & (Gp - 1);
+                tvals[s_] = q[i].v(u);
+                tpart[s_] = (uint16_t)pp[i][u];
             }
-        __syncthreads();  // B3: tile stage complete, in partition order
-        const int ns = off[P - 1] + tcnt[P - 1];
-        for (int s = tid; s < ns; s += TPB) {  // consecutive threads: consecutive rows of a run
-            const int p = tpart[s];
-            const int64_t d = run[p] + (s - off[p]);
-            pkeys[d] = tkeys[s];
-            pvals[d] = tvals[s];
+        __syncthreads();  // B3: stage complete, in partition order
+        const int ns = off[P - 1] + ccnt[P - 1] + tcnt[P - 1];
+        for (int s_ = tid; s_ < ns; s_ += TPB) {  // consecutive threads: consecutive rows of a run
+            const int p = tpart[s_];
+            const int l = lim[p];
+            if (s_ < l) {
+                const int64_t d = dbase[p] + s_;
+                pkeys[d] = tkeys[s_];
+                pvals[d] = tvals[s_];
+            } else {
+                ckeys[p * SW_RUN + (s_ - l)] = tkeys[s_];
+                cvals[p * SW_RUN + (s_ - l)] = tvals[s_];
+            }
         }
         __syncthreads();  // B4: the stage is read
         for (int p = tid; p < P; p += TPB) {
-            run[p] += tcnt[p];
+            const int T = ccnt[p] + tcnt[p];
+            run[p] += fl[p];
+            ccnt[p] = T - fl[p];
             tcnt[p] = 0;
         }
-        // (the next tile's rank atomics come after this thread's reset of its
-        // partitions and before the next B1; other partitions are reset by
-        // their own threads before those threads reach B1)
-        __syncthreads();
+        __syncthreads();  // B5: counts reset before the next tile's ranks
     };
 
     const int64_t nq = (row1 - row0) >> 2;
     const int64_t steps = (nq + TPB * QPT - 1) / (TPB * QPT);
+    const bool vec = ((((uintptr_t)keys) | ((uintptr_t)vals)) & 15) == 0;  // (row0 is a quad multiple)
     QuadT<DT> nxt[QPT];
 #pragma unroll
     for (int i = 0; i < QPT; ++i)
-        if (i * TPB + tid < nq) load_quad<DT, true>(keys, vals, row0 + 4 * (int64_t)(i * TPB + tid), nxt[i]);
+        if (i * TPB + tid < nq) load_quad_rt<DT>(keys, vals, row0 + 4 * (int64_t)(i * TPB + tid), nxt[i], vec);
     for (int64_t s = 0; s < steps; ++s) {
         QuadT<DT> q[QPT];
         uint32_t in[QPT];
@@ -452,7 +568,7 @@ k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__rest
             q[i] = nxt[i];
             in[i] = q0 + (int64_t)i * TPB < nq ? 0xFu : 0u;
             const int64_t qn = q0 + (int64_t)(QPT + i) * TPB;
-            if (qn < nq) load_quad<DT, true>(keys, vals, row0 + 4 * qn, nxt[i]);
+            if (qn < nq) load_quad_rt<DT>(keys, vals, row0 + 4 * qn, nxt[i], vec);
         }
         tile(q, in);
     }
@@ -466,6 +582,15 @@ k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__rest
             in[i] = (i == 0 && tid == 0) ? (1u << tail) - 1u : 0u;
         }
         tile(q, in);
+    }
+    // the last, partial unit of every partition, padded
+    for (int i = tid; i < P * SW_RUN; i += TPB) {
+        const int p = i / SW_RUN, j = i % SW_RUN;
+        if (ccnt[p] > 0) {
+            const int64_t d = run[p] + j;
+            pkeys[d] = j < ccnt[p] ? ckeys[i] : SW_PAD;
+            pvals[d] = j < ccnt[p] ? cvals[i] : V(0);
+        }
     }
 }
 
@@ -489,7 +614,7 @@ k_sweep_acc(const int32_t *__restrict__ pkeys, const typename Fmt<DT>::V *__rest
         if (it >= ctrl[0]) break;
         const int p = (int)items[3 * it];
         const int64_t r0 = items[3 * it + 1], r1 = items[3 * it + 2];
-        Table<DT, K, SW_TPB> tab(smem, s_mm, min(Gp, G - p * Gp), (int64_t)p * Gp, kglob, slots);
+        Table<DT, K, SW_TPB, 0, false, 1> tab(smem, s_mm, min(Gp, G - p * Gp), (int64_t)p * Gp, kglob, slots);
         tab.clear();
         __syncthreads();
         const int64_t nq = (r1 - r0 + 3) >> 2;  // the last quad may hold padding rows
@@ -534,8 +659,8 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
     const SwPlan pl = sw_plan<DT, K>(n, G);
     if (pl.P > SW_PMAX) return -1;
     const size_t sm_cold = sw_smem_cold<DT>();
-    const size_t sm_tab = TabGeom<DT, K>::bytes(pl.Gp);  // accumulate
-    const size_t sm_hot = TabGeom<DT, K>::bytes(pl.Gp, TAB_HMAX);  // hot pass (+ heavy-group lane copies)
+    const size_t sm_tab = TabGeom<DT, K, 1>::bytes(pl.Gp);  // accumulate
+    const size_t sm_hot = TabGeom<DT, K, 1>::bytes(pl.Gp, TAB_HMAX);  // hot pass (+ heavy-group lane copies)
     if (sm_hot > (size_t)device_props().smem_optin - 1024) return -1;
     SwWs w = sw_carve<DT, K>(ws, n, G, pl);
     if (w.bytes > ws_bytes) return -1;
@@ -560,13 +685,14 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
         int64_t chunk = (n + pl.grid - 1) / pl.grid;
         chunk = (chunk + 3) & ~(int64_t)3;
         const int grid = (int)((n + chunk - 1) / chunk);
+        const ColdSrc cs{w.hcnt, grid, chunk};
         rc = traced("sweep_hot", st, launches, [&] {  // returns at once when no partition is hot
             k_sweep_hot<DT, K><<<grid, SW_HTPB, sm_hot, st>>>(keys, (const V *)vals, n, G, pl.gbits, chunk, w.bkeys,
-                                                             (V *)w.bvals, w.ctrl, w.kglob, w.slots, status);
+                                                             (V *)w.bvals, w.ctrl, w.hcnt, w.kglob, w.slots, status);
         });
         if (rc) return rc;
         rc = traced("sweep_hist", st, launches, [&] {
-            k_sw_hist<<<pl.cgrid, SW_CTPB, 0, st>>>(keys, w.bkeys, n, G, pl.gbits, pl.P, w.ctrl, w.cnt, status);
+            k_sw_hist<<<pl.cgrid, SW_CTPB, 0, st>>>(keys, w.bkeys, n, G, pl.gbits, pl.P, w.ctrl, cs, w.cnt, status);
         });
         if (rc) return rc;
         rc = traced("sweep_scan", st, launches, [&] {
@@ -574,9 +700,9 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
         });
         if (rc) return rc;
         rc = traced("sweep_scatter", st, launches, [&] {
-            k_sweep_cold<DT><<<pl.cgrid, SW_CTPB, sm_cold, st>>>(keys, (const V *)vals, n, w.bkeys,
+            k_sweep_cold<DT><<<pl.cgrid, SW_STPB, sm_cold, st>>>(keys, (const V *)vals, n, w.bkeys,
                                                                  (const V *)w.bvals, G, pl.gbits, pl.P, w.cnt,
-                                                                 w.pkeys, (V *)w.pvals, w.ctrl);
+                                                                 w.pkeys, (V *)w.pvals, w.ctrl, cs);
         });
         if (rc) return rc;
         rc = traced("sweep_accumulate", st, launches, [&] {

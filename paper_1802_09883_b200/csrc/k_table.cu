@@ -32,6 +32,12 @@
 //     with k* > kuni is deposited straight into the slot table at its own
 //     window k* (and raises the group's global top), which is exact for the
 //     same reason.
+//   * band mode (the > 2048-group kernel only, Table XB = 1): a block whose
+//     groups still differ in top after the first tile streams with every row
+//     at its own window over K + 1 levels (table_core.cuh) until every group
+//     reached the top.  The <= 2048-group kernels stay block-synchronous in
+//     that case: compiled into their loop, the band mode cost the uniform
+//     mode -- config 1 -- 4-5% (registers).
 // Rows with a key outside [0, G) or a NaN/Inf/ERANGE value set the status
 // bits (precedence EKEY > EDOM > ERANGE on read) and deposit nothing.
 #include "common.cuh"
@@ -51,11 +57,19 @@ namespace {
 #ifndef TAB_L2PF
 #define TAB_L2PF 0  // (measured slower: 0.419 -> 0.461 ms at 3 steps) steps ahead whose rows lane 0 of each warp prefetches into L2 (0: off)
 #endif
+
+#ifndef TAB_OBS2
+#define TAB_OBS2 0  // 1: counters observed on every other step only (red.shared in between; TPB <= 256)
+#endif
 #ifndef TAB_MINB256
 #define TAB_MINB256 2  // resident 256-thread blocks per SM the register budget is sized for
 #endif
 
-template <int DT, int K, int TPB, bool VEC, int GQC>
+#if TAB_DEBUG
+__device__ unsigned long long g_tab_modes[3];
+#endif
+
+template <int DT, int K, int TPB, bool VEC, int GQC, int XB>
 __global__ void __launch_bounds__(TPB, TPB == 256 ? TAB_MINB256 : 1)
 k_table(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals, int64_t n, int32_t G,
         int64_t chunk, int32_t *__restrict__ kglob, unsigned long long *__restrict__ slots,
@@ -66,7 +80,7 @@ k_table(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict_
     const int64_t row0 = (int64_t)blockIdx.x * chunk;
     const int64_t row1 = min(n, row0 + chunk);
     if (row0 >= row1) return;
-    Table<DT, K, TPB, GQC> tab(smem, s_mm, G, 0, kglob, slots);
+    Table<DT, K, TPB, GQC, false, XB> tab(smem, s_mm, G, 0, kglob, slots);
     tab.clear();
     uint32_t flags = 0;
     __syncthreads();
@@ -81,7 +95,8 @@ k_table(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict_
 #pragma unroll
     for (int i = 0; i < QPT; ++i)
         if (i * TPB + tid < nq) load_quad<DT, VEC>(keys, vals, row0 + 4 * (int64_t)(i * TPB + tid), nxt[i]);
-    for (int64_t s = 0; s < steps; ++s) {  // block-uniform trip count
+    // one step: the next step's quads are issued, this step's deposited
+    auto step = [&](int64_t s, auto &&deposit) {
         QuadT<DT> cur[QPT];
 #pragma unroll
         for (int i = 0; i < QPT; ++i) cur[i] = nxt[i];
@@ -106,30 +121,49 @@ k_table(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict_
             }
         }
 #pragma unroll
-        for (int i = 0; i < QPT; ++i) tab.quad(cur[i], q0 + (int64_t)i * TPB < nq ? 0xFu : 0u, flags);
+        for (int i = 0; i < QPT; ++i)
+            deposit(cur[i], q0 + (int64_t)i * TPB < nq ? 0xFu : 0u, !TAB_OBS2 || ((s * QPT + i) & 1) == 0);
+    };
+    int64_t s = 0;
+    if (XB > 0) {
+        // phases (block-uniform): block-synchronous / band mode until the
+        // table streams in the uniform mode, then a loop with the uniform
+        // deposit only (with the band mode compiled into the loop, one loop
+        // for all modes costs the uniform mode ~4%; without it, the single
+        // loop is the faster one)
+        for (; s < steps && !tab.uniform(); ++s)  // block-uniform trip count
+            step(s, [&](const QuadT<DT> &q, uint32_t in, bool obs) { tab.quad(q, in, flags, obs); });
+        for (; s < steps; ++s)
+            step(s, [&](const QuadT<DT> &q, uint32_t in, bool obs) { tab.fast_quad(q, in, flags, obs); });
+    } else {
+        for (; s < steps; ++s)
+            step(s, [&](const QuadT<DT> &q, uint32_t in, bool obs) { tab.quad(q, in, flags, obs); });
     }
-    // tail (< 4 rows, last block only), block-synchronous
+    // tail (< 4 rows, last block only)
     const int tail = (int)(row1 - row0 - 4 * nq);
     if (tail > 0) {  // block-uniform
         QuadT<DT> t;
         load_partial<DT>(keys, vals, row0 + 4 * nq, tid == 0 ? tail : 0, t);
-        tab.slow_quad(t, tid == 0 ? (1u << tail) - 1u : 0u, flags);
+        tab.quad(t, tid == 0 ? (1u << tail) - 1u : 0u, flags);
     }
     tab.finish();
+#if TAB_DEBUG
+    tab.dbg_flush(g_tab_modes);
+#endif
     flags = __reduce_or_sync(0xffffffffu, flags);
     if ((tid & 31) == 0 && flags) atomicOr(status, flags);
 }
 
-template <int DT, int K, int TPB, int GQC>
+template <int DT, int K, int TPB, int GQC, int XB>
 int launch_table_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, int32_t *kglob,
                    unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches) {
-    using Geo = TabGeom<DT, K>;
+    using Geo = TabGeom<DT, K, XB>;
     using V = typename Fmt<DT>::V;
-    const size_t smem = GQC > 0 ? (size_t)GQC * (4 * Geo::CW + 12) : Geo::bytes(G);
+    const size_t smem = GQC > 0 ? Geo::bytes_gqc(GQC) : Geo::bytes(G);
     if (GQC > 0 && Geo::gq(G) > GQC) return -1;
     if (smem > (size_t)device_props().smem_optin) return -1;
     const bool vec = (((uintptr_t)keys | (uintptr_t)vals) & 15) == 0;
-    auto kern = vec ? k_table<DT, K, TPB, true, GQC> : k_table<DT, K, TPB, false, GQC>;
+    auto kern = vec ? k_table<DT, K, TPB, true, GQC, XB> : k_table<DT, K, TPB, false, GQC, XB>;
     static thread_local size_t configured[2] = {};
     if (configured[vec] < smem) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
@@ -161,9 +195,11 @@ int launch_table_any(int DT, int K, const int32_t *keys, const void *vals, int64
                      unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches) {
 #define TAB_CASE(dt, k)                                                                                   \
     if (DT == dt && K == k)                                                                               \
-        return G <= 1024 ? launch_table_t<dt, k, 256, 1028>(keys, vals, n, G, kglob, slots, status, st, launches) \
-             : G <= 2048 ? launch_table_t<dt, k, 256, 0>(keys, vals, n, G, kglob, slots, status, st, launches)    \
-                         : launch_table_t<dt, k, 512, 0>(keys, vals, n, G, kglob, slots, status, st, launches);
+        return G <= 1024 ? launch_table_t<dt, k, 256, 1028, 0>(keys, vals, n, G, kglob, slots, status, st, launches) \
+             : G <= 2048 ? launch_table_t<dt, k, 256, 0, 0>(keys, vals, n, G, kglob, slots, status, st, launches)    \
+             : TabGeom<dt, k, 1>::bytes(G) <= (size_t)device_props().smem_optin - 1024                              \
+                         ? launch_table_t<dt, k, 512, 0, 1>(keys, vals, n, G, kglob, slots, status, st, launches)   \
+                         : launch_table_t<dt, k, 512, 0, 0>(keys, vals, n, G, kglob, slots, status, st, launches);
     TAB_CASE(1, 1) TAB_CASE(1, 2) TAB_CASE(1, 3) TAB_CASE(1, 4)
     TAB_CASE(0, 1) TAB_CASE(0, 2) TAB_CASE(0, 3) TAB_CASE(0, 4)
 #undef TAB_CASE
@@ -171,3 +207,14 @@ int launch_table_any(int DT, int K, const int32_t *keys, const void *vals, int64
 }
 
 }  // namespace repro
+
+#if TAB_DEBUG
+// debug builds: calls per table mode of k_table since the last read (slow, band, uniform)
+extern "C" int repro_debug_table_modes(unsigned long long *out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, repro::g_tab_modes, sizeof(unsigned long long) * 3);
+    const unsigned long long z[3] = {0, 0, 0};
+    cudaMemcpyToSymbol(repro::g_tab_modes, z, sizeof(z));
+    return 0;
+}
+#endif

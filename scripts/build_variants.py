@@ -14,7 +14,8 @@ spec.loader.exec_module(bn)
 out = os.path.join(ROOT, "scripts", "variants")
 os.makedirs(out, exist_ok=True)
 for f in os.listdir(out):
-    os.remove(os.path.join(out, f))
+    if os.path.isfile(os.path.join(out, f)):
+        os.remove(os.path.join(out, f))
 
 
 def one(arg):

@@ -1,0 +1,11 @@
+#!/bin/bash
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out/r2f
+REPRO_B200_LIB=$PWD/scripts/variants/lib_tb.so timeout 900 python -m pytest tests/test_gpu_band.py tests/test_gpu_parity.py -x -q -p no:cacheprovider -k "band or partitioned or table or random or config0" > gpurun_out/r2f/tests.txt 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/r2f/tests.txt
+B="python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-atomic-baseline --no-configs --no-e2e --no-parity"
+for v in tb tb0 s4k s4kq; do
+for c in "--config 1" "--config 2 --n-groups 4096" "--config 2 --n-groups 1024" "--config 3" "--config 2 --n-groups 1048576" "--config 2 --n-groups 65536"; do
+  REPRO_B200_LIB=$PWD/scripts/variants/lib_$v.so timeout 600 $B $c > gpurun_out/r2f/b.json 2>gpurun_out/r2f/b.err
+  python -c "import json; d=json.load(open('gpurun_out/r2f/b.json')); print('$v $c', round(d['ms_per_step'],4), {k: round(v,4) for k,v in d['per_kernel_ms'].items()})" || tail -3 gpurun_out/r2f/b.err
+done
+done

@@ -51,3 +51,21 @@ def test_sparse_capacity_and_errors(R):
     assert e.value.status == R.EKEY
     uk, out = R.groupby_sum_sparse(dev(np.zeros(0, np.int64)), dev(np.zeros(0)), max_groups=10)
     assert uk.numel() == 0 and out.numel() == 0
+
+
+@pytest.mark.parametrize("dtype,distinct,n,K", [(np.float64, 500, 300007, 3), (np.float32, 30000, 400001, 2)])
+def test_sparse_int32_keys_match_oracle(R, dtype, distinct, n, K):
+    # every int32 value is a valid key (INT32_MIN included); out_keys int64
+    rng = np.random.default_rng(distinct)
+    pool = np.unique(np.concatenate([[np.iinfo(np.int32).min, np.iinfo(np.int32).max, 0, -1],
+                                     rng.integers(-(1 << 31), (1 << 31) - 1, distinct * 2)]))[:distinct]
+    keys = pool[rng.integers(0, pool.size, n)].astype(np.int32)
+    vals = (rng.standard_normal(n) * 2.0 ** rng.integers(-20, 20, n)).astype(dtype)
+    uk, out = R.groupby_sum_sparse(dev(keys), dev(vals), max_groups=2 * distinct, fold=K)
+    rc, ruk, rout = O.groupby_sum_sparse(keys.astype(np.int64), vals, K)
+    assert rc == O.OK
+    assert uk.dtype == torch.int64 and np.array_equal(uk.cpu().numpy(), ruk)
+    assert out.cpu().numpy().tobytes() == rout.tobytes()
+    # the same multiset as int64 keys gives the same bits
+    uk64, out64 = R.groupby_sum_sparse(dev(keys.astype(np.int64)), dev(vals), max_groups=2 * distinct, fold=K)
+    assert torch.equal(uk, uk64) and torch.equal(out, out64)
