@@ -477,6 +477,14 @@ void repro_set_path_override(int32_t path);
  * bits. */
 void repro_set_kernel_variant(int32_t variant);
 
+/* Routed one-pass kernel of the partitioned path (k_route.cu), opt-in:
+ * 1 on (used whenever the groups fit the SMs' shared-memory tables, about 1M
+ * binary64 K=3 groups on 148 SMs), 0 off (default: the two-pass sweep runs;
+ * the routed kernel measured slower on B200).  Rows move to the SM that owns their group through small L2
+ * ring buffers (PartitionAndAggregate, with the partitions
+ * streamed instead of materialised).  Never changes result bits. */
+void repro_set_route_mode(int32_t mode);
+
 /* Per-kernel device timing (benchmark aid).  While enabled, every kernel the
  * library enqueues from this host thread is bracketed by a CUDA event pair
  * recorded on the launching stream. */

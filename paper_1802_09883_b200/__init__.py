@@ -102,6 +102,7 @@ _sig("repro_onchip_max_groups", _i32, _i32, _i32)
 _sig("repro_sweep_max_groups", _i32, _i32, _i32)
 _sig("repro_set_path_override", None, _i32)
 _sig("repro_set_kernel_variant", None, _i32)
+_sig("repro_set_route_mode", None, _i32)
 _sig("repro_timing_enable", None, _i32)
 _sig("repro_timing_collect", _i32, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(_i32),
      ctypes.POINTER(ctypes.c_double), _i32)
@@ -621,6 +622,13 @@ def set_kernel_variant(variant: int):
     """0 auto, 1 per-row atomics fed by the TMA ring, 2 k_table (register-fed
     counter table), 3 per-row atomics with register loads (bits never change)."""
     _lib.repro_set_kernel_variant(variant)
+
+
+def set_route_mode(mode: int):
+    """1: the routed one-pass kernel where the groups fit the SMs' tables
+    (opt-in, measured slower); 0 (default): the two-pass sweep.  Bits never
+    change."""
+    _lib.repro_set_route_mode(mode)
 
 
 def timing_enable(on: bool = True):

@@ -106,6 +106,7 @@ constexpr size_t ALIGN = 256;
 inline size_t align_up(size_t x) { return (x + ALIGN - 1) / ALIGN * ALIGN; }
 
 int status_from_flags(uint32_t f) {
+    if (f & FLAG_ESTALL) return REPRO_ECUDA;
     if (f & FLAG_EINVAL) return REPRO_EINVAL;
     if (f & FLAG_EKEY) return REPRO_EKEY;
     if (f & FLAG_EDOM) return REPRO_EDOM;
@@ -344,6 +345,7 @@ int32_t repro_sweep_max_groups(int32_t fold, int32_t dtype) {
     return sweep_max_groups(fold, dtype);
 }
 void repro_set_kernel_variant(int32_t variant) { set_onchip_variant(variant); }
+void repro_set_route_mode(int32_t mode) { set_route_mode(mode); }
 
 void repro_timing_enable(int32_t on) { t_timing = on != 0; }
 

@@ -23,7 +23,9 @@
 namespace repro {
 
 // device status word bits (OR-ed; precedence EKEY > EDOM > ERANGE on read)
-enum : uint32_t { FLAG_EKEY = 1u, FLAG_EDOM = 2u, FLAG_ERANGE = 4u, FLAG_EINVAL = 8u };
+// FLAG_ESTALL: a cross-block wait of the routed path (k_route.cu) gave up
+// (reported as REPRO_ECUDA; never expected)
+enum : uint32_t { FLAG_EKEY = 1u, FLAG_EDOM = 2u, FLAG_ERANGE = 4u, FLAG_EINVAL = 8u, FLAG_ESTALL = 16u };
 
 template <int DT>
 struct Fmt;

@@ -133,6 +133,15 @@ int launch_sweep(int DT, int K, const int32_t *keys, const void *vals, int64_t n
                  size_t ws_bytes, int merge, int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *out,
                  uint32_t *status, cudaStream_t st, int *launches);
 
+// ---- routed one-pass path (k_route.cu): rows move to their group's SM
+// through L2 rings; -1 when the shape does not apply (the sweep runs)
+void set_route_mode(int m);  // 0 off, 1 auto
+int route_mode();
+size_t route_workspace_bytes(int32_t G, int K, int DT);
+int launch_route(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G, void *ws,
+                 size_t ws_bytes, int merge, int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *out,
+                 uint32_t *status, cudaStream_t st, int *launches);
+
 // ---- NVLS (multimem) all-reduce of a slot table (k_nvls.cu) --------------
 int launch_nvls_reduce(uint32_t *mc_flags, int32_t *mc_kglob, int64_t nk, unsigned long long *mc_slots, int64_t ns,
                        int rank, int world, cudaStream_t st, int *launches);

@@ -245,7 +245,7 @@ k_limbs_finalize(int32_t count, const int32_t *__restrict__ kg, const int64_t *_
 
 __global__ void k_status(const uint32_t *flags, int32_t *d_status) {
     const uint32_t f = *flags;
-    d_status[0] = (f & FLAG_EINVAL) ? -1 : (f & FLAG_EKEY) ? -2 : (f & FLAG_EDOM) ? -3 : (f & FLAG_ERANGE) ? -4 : 0;
+    d_status[0] = (f & FLAG_ESTALL) ? -5 : (f & FLAG_EINVAL) ? -1 : (f & FLAG_EKEY) ? -2 : (f & FLAG_EDOM) ? -3 : (f & FLAG_ERANGE) ? -4 : 0;
 }
 
 inline unsigned blocks_for(int64_t n) { return (unsigned)((n + TPB_STATE - 1) / TPB_STATE); }

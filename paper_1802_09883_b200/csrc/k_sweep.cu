@@ -7,7 +7,8 @@
 // (Gp sized so that one partition's table fits on chip: F = f^d with d = 1,
 // PAPER.md:1054-1058).
 //   1. k_sw_sample  8192 evenly spaced keys; a partition holding >= 1/8 of
-//                   them is HOT (skew, e.g. Zipf's head).
+//                   them and >= 4x its uniform share is HOT (skew, e.g.
+//                   Zipf's head).
 //   2. k_sweep_hot  (hot partition only) one pass over the rows: hot rows are
 //                   deposited on chip right away (table_core.cuh; the heavy
 //                   partition never goes back to HBM), the others are
@@ -218,7 +219,10 @@ __global__ void __launch_bounds__(1024) k_sw_sample(const int32_t *__restrict__ 
     const int samples = (int)min((int64_t)SW_SAMPLE, n);
     if (tid == 0) {
         const int c = (int)(best >> 32);
-        s_hot = (c > 0 && 8 * c >= samples) ? SW_PMAX - 1 - (int)(best & 0xFFFFFFFFu) : -1;
+        // hot: >= 1/8 of the samples AND >= 4x a partition's uniform share
+        // (uniform keys over a few partitions are cheaper through the scatter)
+        s_hot = (c > 0 && 8 * c >= samples && (int64_t)c * P >= 4 * (int64_t)samples)
+                    ? SW_PMAX - 1 - (int)(best & 0xFFFFFFFFu) : -1;
         ctrl[3] = s_hot;
         ctrl[5] = 0;
     }
@@ -656,6 +660,10 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
                    int merge, int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *out, uint32_t *status,
                    cudaStream_t st, int *launches) {
     using V = typename Fmt<DT>::V;
+    // one pass through L2 rings when the groups fit the SMs' tables
+    const int rr = launch_route(DT, K, keys, vals, n, G, ws, ws_bytes, merge, acc_k, acc_C, acc_D, out, status, st,
+                                launches);
+    if (rr != -1) return rr;
     const SwPlan pl = sw_plan<DT, K>(n, G);
     if (pl.P > SW_PMAX) return -1;
     const size_t sm_cold = sw_smem_cold<DT>();
@@ -729,7 +737,7 @@ size_t sweep_workspace_bytes(int64_t n, int32_t G, int K, int DT) {
 #define SWB(dt, k)                                          \
     if (DT == dt && K == k) {                               \
         const SwPlan pl = sw_plan<dt, k>(n, G);             \
-        return sw_carve<dt, k>(nullptr, n, G, pl).bytes;    \
+        return std::max(sw_carve<dt, k>(nullptr, n, G, pl).bytes, route_workspace_bytes(G, k, dt)); \
     }
     SWB(1, 1) SWB(1, 2) SWB(1, 3) SWB(1, 4) SWB(0, 1) SWB(0, 2) SWB(0, 3) SWB(0, 4)
 #undef SWB

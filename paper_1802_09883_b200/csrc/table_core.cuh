@@ -21,7 +21,10 @@ constexpr int TAB_HMAX = 32;
 #define TAB_DEBUG 0  // count the calls per table mode (repro_debug_table_modes; debug builds only)
 #endif
 #ifndef TAB_BAND_CHECK
-#define TAB_BAND_CHECK 4  // band-mode calls between checks for the switch to the uniform mode
+#define TAB_BAND_CHECK 4  // band-mode calls before the first check for the switch to the uniform mode
+#endif
+#ifndef TAB_BAND_CHECK_MAX
+#define TAB_BAND_CHECK_MAX 1024  // the interval doubles after every check that fails (skewed keys: never)
 #endif
 #ifndef TAB_VOTE_LO
 #define TAB_VOTE_LO 1  // vote on the low limbs of binary64 digits too (skip a position the warp leaves at zero)
@@ -198,6 +201,7 @@ struct Table {
     bool first;
     bool band;      // band mode (XB = 1; block-uniform)
     int bcalls;     // band_quad calls since the last switch check (block-uniform)
+    int bcheck;     // calls between switch checks (doubles after each failed check)
     int par;  // parity of slow_quad calls (block-uniform)
     int nh;           // heavy groups (HH)
     int8_t *hmap;     // local group -> heavy index or -1 (HH, shared, G entries)
@@ -207,7 +211,7 @@ struct Table {
     __device__ __forceinline__ Table(unsigned char *mem, int *mm, int G_, int64_t gbase_, int32_t *kglob_,
                                      unsigned long long *slots_, int nh_ = 0)
         : s_mm(mm), G(G_), gbase(gbase_), kglob(kglob_), slots(slots_), kuni(-1), lim(0), mlim(0), llim(0), big(0),
-          first(true), band(false), bcalls(0), par(0), nh(HH ? nh_ : 0), ex(0) {
+          first(true), band(false), bcalls(0), bcheck(TAB_BAND_CHECK), par(0), nh(HH ? nh_ : 0), ex(0) {
         gq = GQC > 0 ? GQC : Geo::gq(G, nh);
         // (GQC > 0: the per-group int arrays are GQC long too -- compile-time
         // offsets; a G-dependent length costs the hot loop registers)
@@ -235,6 +239,7 @@ struct Table {
         first = true;
         band = false;
         bcalls = 0;
+        bcheck = TAB_BAND_CHECK;
     }
     // set the heavy groups (HH; after clear() and a barrier, before a barrier)
     __device__ __forceinline__ void set_heavy(const int32_t *keys_local, int count) {
@@ -480,12 +485,16 @@ struct Table {
             exc &= exc - 1;
             exceptional(kq(q.k, u), q.v(u), flags);
         }
-        // every TAB_BAND_CHECK calls: once every group has reached kuni, the
-        // uniform mode takes over (same counter words; block-uniform decision)
-        if (++bcalls == TAB_BAND_CHECK) {
+        // once every group has reached kuni, the uniform mode takes over
+        // (same counter words; block-uniform decision).  Checked after
+        // TAB_BAND_CHECK calls, then at doubling intervals: with skewed keys
+        // some groups may never reach the top, and each check is a barrier
+        if (++bcalls == bcheck) {
             bcalls = 0;
             if (__syncthreads_and(ld_shared_u32((uint32_t)__cvta_generic_to_shared(&s_mm[NTOP])) >= (uint32_t)G))
                 band = false;
+            else
+                bcheck = min(2 * bcheck, TAB_BAND_CHECK_MAX);
         }
     }
 
@@ -563,6 +572,7 @@ struct Table {
                 set_window(kb);
                 band = true;
                 bcalls = 0;
+                bcheck = TAB_BAND_CHECK;
             }
         }
         __syncthreads();  // raise phase done / the list length is reset before the next call's appends
