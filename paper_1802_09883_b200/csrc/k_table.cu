@@ -52,15 +52,18 @@ namespace repro {
 namespace {
 
 #ifndef TAB_QPT
-#define TAB_QPT 1  // quads (4 rows) per thread per step; the next step's are in flight
+#define TAB_QPT 2  // quads (4 rows) per thread per step (256-thread kernels); the next step's are in flight
+#endif
+#ifndef TAB_QPT512
+#define TAB_QPT512 1  // the same for the 512-thread (> 2048 groups) kernels
 #endif
 #ifndef TAB_L2PF
 #define TAB_L2PF 0  // (measured slower: 0.419 -> 0.461 ms at 3 steps) steps ahead whose rows lane 0 of each warp prefetches into L2 (0: off)
 #endif
 
 #ifndef TAB_OBS2
-#define TAB_OBS2 0  // 1: counters observed on every other step only (red.shared in between; TPB <= 256)
-#endif
+#define TAB_OBS2 1  // 1: counters observed on every other quad only (red.shared in between; TPB <= 256)
+#endif  // (config 1, 2^27 rows: QPT 1 / OBS2 0 0.419 ms, QPT 2 + OBS2 0.406 ms; each alone is slower)
 #ifndef TAB_MINB256
 #define TAB_MINB256 2  // resident 256-thread blocks per SM the register budget is sized for
 #endif
@@ -89,7 +92,7 @@ k_table(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict_
     const int64_t nq = (row1 - row0) >> 2;
     // software pipeline: the next step's quads are in flight while this
     // step's are deposited (quad i of step s: q = (s QPT + i) TPB + tid)
-    constexpr int QPT = TAB_QPT;
+    constexpr int QPT = TPB == 256 ? TAB_QPT : TAB_QPT512;
     QuadT<DT> nxt[QPT];
     const int64_t steps = (nq + TPB * QPT - 1) / (TPB * QPT);
 #pragma unroll
