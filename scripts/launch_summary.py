@@ -16,8 +16,8 @@ for r in rows[hdr + 1:]:
         name = r[ki].split("(")[0].replace("void ", "").replace("repro::", "").replace("<unnamed>::", "")
         name = name.replace("unnamed>::", "").lstrip("<")
         agg[name].append(float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0))
-def aside(k):  # not part of the timed step: the atomicAdd baseline, input generation, torch fills
-    return "k_base" in k or "k_synth" in k or k.startswith("at::")
+def aside(k):  # not part of the timed step: the atomicAdd baseline, input generation, the FP-rate probe, torch fills
+    return "k_base" in k or "k_synth" in k or "k_fp_add_peak" in k or k.startswith("at::")
 
 
 step = {k: v for k, v in agg.items() if not aside(k)}
@@ -27,6 +27,6 @@ for k, v in sorted(step.items(), key=lambda kv: -sum(kv[1])):
     print(f"{k[:48]:48s} {len(v):8d} {sum(v) / len(v):10.2f} {sum(v) / total:13.3f}")
 base = {k: v for k, v in agg.items() if aside(k)}
 if base:
-    print("# not part of the step (atomicAdd baseline, input generator, torch fills):")
+    print("# not part of the step (atomicAdd baseline, input generator, FP add-rate probe, torch fills):")
     for k, v in base.items():
         print(f"{k[:48]:48s} {len(v):8d} {sum(v) / len(v):10.2f}")
