@@ -275,37 +275,48 @@ k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restr
     tab.set_heavy(ctrl + 8, nh);
     uint32_t flags = 0;
     __syncthreads();
+    const uint32_t lt = (1u << lane) - 1u;
     auto step = [&](const QuadT<DT> &q, uint32_t in) {
-        uint32_t hin = 0, cin = 0;
+        // branch-free classification: hot rows (hin) go to the table, cold
+        // rows (cin) to the compacted buffer, bad keys set EKEY
+        uint32_t hin = 0, cin = 0, bad = 0;
         int hk[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int32_t k = kq(q.k, u);
-            hk[u] = 0;
-            if (!((in >> u) & 1u)) continue;
-            if ((uint32_t)k >= (uint32_t)G) { flags |= FLAG_EKEY; continue; }
-            if ((k >> gbits) == hot) { hin |= 1u << u; hk[u] = k & (Gp - 1); }
-            else cin |= 1u << u;
+            const bool iu = (in >> u) & 1u;
+            const bool ok = (uint32_t)k < (uint32_t)G;
+            const bool h = ok && (k >> gbits) == hot;
+            hin |= (iu && h) ? 1u << u : 0u;
+            cin |= (iu && ok && !h) ? 1u << u : 0u;
+            bad |= (iu && !ok) ? 1u : 0u;
+            hk[u] = k & (Gp - 1);
         }
-        // compaction: the warp's cold rows go to one reserved run of the
-        // block's region (a shared counter: no global contention)
-        const int c = __popc(cin);
-        int pre = c;
+        if (bad) flags |= FLAG_EKEY;
+        // compaction: one ballot per quad slot; the warp's cold rows of slot u
+        // land in consecutive positions (coalesced stores), one shared atomic
+        // per warp reserves them in the block's region
+        uint32_t m[4];
+        int tot = 0;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(0xffffffffu, pre, o);
-            if (lane >= o) pre += y;
+        for (int u = 0; u < 4; ++u) {
+            m[u] = __ballot_sync(0xffffffffu, (cin >> u) & 1u);
+            tot += __popc(m[u]);
         }
-        int base = 0;
-        if (lane == 31 && pre > 0) base = atomicAdd(&s_ccount, pre);
-        int64_t pos = row0 + __shfl_sync(0xffffffffu, base, 31) + pre - c;
+        if (tot) {  // (warp-uniform)
+            int base = 0;
+            if (lane == 0) base = atomicAdd(&s_ccount, tot);
+            base = __shfl_sync(0xffffffffu, base, 0);
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if ((cin >> u) & 1u) {
-                bkeys[pos] = kq(q.k, u);
-                bvals[pos] = q.v(u);
-                ++pos;
+            for (int u = 0; u < 4; ++u) {
+                if ((cin >> u) & 1u) {
+                    const int64_t pos = row0 + base + __popc(m[u] & lt);
+                    bkeys[pos] = kq(q.k, u);
+                    bvals[pos] = q.v(u);
+                }
+                base += __popc(m[u]);
             }
+        }
         QuadT<DT> hq = q;
         hq.k = make_int4(hk[0], hk[1], hk[2], hk[3]);
         tab.quad(hq, hin, flags);

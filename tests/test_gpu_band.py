@@ -127,3 +127,39 @@ def test_hot_partition_band_with_heavy_groups(R):
     vals = (rng.standard_normal(n) * np.exp2(rng.integers(-10, 11, n))).astype(np.float32)
     run(R, keys, vals, G, 2)
     assert R.last_path() == 1
+
+
+@pytest.mark.parametrize("bad", [-1, "G", "big"])
+def test_hot_partition_pass_bad_keys(R, bad):
+    # the hot pass classifies every row (hot / cold / bad key): a bad key
+    # anywhere (in a hot block, late in the input) is EKEY, as in the oracle
+    rng = np.random.default_rng(21)
+    G, n = 1 << 20, (1 << 21) + 7
+    keys = zipf_keys(rng, n, G)
+    vals = (rng.standard_normal(n) * np.exp2(rng.integers(-10, 11, n))).astype(np.float32)
+    keys[n - 5] = {-1: -1, "G": G, "big": 2 ** 31 - 1}[bad]
+    assert O.groupby_sum(keys, vals, G, 2)[0] == O.EKEY
+    with pytest.raises(R.ReproError) as ei:
+        R.groupby_sum(torch.from_numpy(keys).cuda(), torch.from_numpy(vals).cuda(), G, 2)
+    torch.cuda.synchronize()
+    assert ei.value.status == O.EKEY
+
+
+@pytest.mark.parametrize("offset", [1, 3])
+def test_hot_partition_pass_unaligned(R, offset):
+    # row arrays that are not 16-byte aligned take the scalar loads; the
+    # compacted cold rows and the hot table must not care
+    rng = np.random.default_rng(offset + 40)
+    G, n = 1 << 20, (1 << 21) + 3
+    keys = zipf_keys(rng, n, G)
+    vals = (rng.standard_normal(n) * np.exp2(rng.integers(-10, 11, n))).astype(np.float32)
+    kt = torch.zeros(n + offset, dtype=torch.int32, device="cuda")
+    vt = torch.zeros(n + offset, dtype=torch.float32, device="cuda")
+    kt[offset:] = torch.from_numpy(keys).cuda()
+    vt[offset:] = torch.from_numpy(vals).cuda()
+    out = R.groupby_sum(kt[offset:], vt[offset:], G, 2)
+    torch.cuda.synchronize()
+    rc, ref = O.groupby_sum(keys, vals, G, 2)
+    assert rc == O.OK
+    assert out.cpu().numpy().view(np.uint32).tobytes() == ref.view(np.uint32).tobytes()
+    assert R.last_path() == 1
