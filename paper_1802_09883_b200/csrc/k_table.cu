@@ -191,14 +191,14 @@ int launch_table_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
 int table_max_groups(int K, int DT) {
     const size_t cap = (size_t)device_props().smem_optin;
     const size_t per = 4 * (size_t)K * (DT == 1 ? 2 : 1) + 12;
-    return (int)((cap - 64 - 1024) / per) - 8;  // (static shared memory comes out of the same budget)
+    return (int)((cap - 64 - 1024) / per) - 8 - 32;  // (static shared memory comes out of the same budget; lane sinks)
 }
 
 int launch_table_any(int DT, int K, const int32_t *keys, const void *vals, int64_t n, int32_t G, int32_t *kglob,
                      unsigned long long *slots, uint32_t *status, cudaStream_t st, int *launches) {
 #define TAB_CASE(dt, k)                                                                                   \
     if (DT == dt && K == k)                                                                               \
-        return G <= 1024 ? launch_table_t<dt, k, 256, 1028, 0>(keys, vals, n, G, kglob, slots, status, st, launches) \
+        return G <= 1024 ? launch_table_t<dt, k, 256, 1056, 0>(keys, vals, n, G, kglob, slots, status, st, launches) \
              : G <= 2048 ? launch_table_t<dt, k, 256, 0, 0>(keys, vals, n, G, kglob, slots, status, st, launches)    \
              : TabGeom<dt, k, 1>::bytes(G) <= (size_t)device_props().smem_optin - 1024                              \
                          ? launch_table_t<dt, k, 512, 0, 1>(keys, vals, n, G, kglob, slots, status, st, launches)   \

@@ -17,6 +17,9 @@ constexpr uint32_t TAB_DRAIN_BIAS = 0x20000000u;  // |old| >= 2^29  <=>  (old + 
 constexpr uint32_t TAB_DRAIN_MASK = 0xC0000000u;
 constexpr int TAB_MM = 64;  // shared control words of a Table: lists, tops, rows per k* (first tile), NTOP
 constexpr int TAB_HMAX = 32;
+// rows that are not deposited add zeros into a SINK column of their own lane
+// (G + lane: bank = lane), so that they never pile up on one shared word
+constexpr int TAB_SINKS = 32;
 #ifndef TAB_DEBUG
 #define TAB_DEBUG 0  // count the calls per table mode (repro_debug_table_modes; debug builds only)
 #endif
@@ -132,9 +135,9 @@ __device__ __forceinline__ int64_t counter_part(int w, uint32_t c) {
 }
 
 // Shared memory of a table of G groups: counters u32 [CWB][gq], ktop int32
-// [gr], knext int32 [gr], raised-group list int32 [gr]; gq = G + 1 (a sink
-// group that receives the zero limbs of skipped rows) + the heavy groups' lane
-// copies, rounded to 4; gr = G + 1 rounded to 4.  CWB = (K + XB) * LIMBS
+// [gr], knext int32 [gr], raised-group list int32 [gr]; gq = G + TAB_SINKS
+// (one sink column per lane for the zero limbs of skipped rows) + the heavy
+// groups' lane copies, rounded to 4; gr = G + 1 rounded to 4.  CWB = (K + XB) * LIMBS
 // counter words per group: XB = 1 adds one level below the window for the
 // band mode (Table::band_quad).
 template <int DT, int K, int XB = 0>
@@ -142,7 +145,7 @@ struct TabGeom {
     static constexpr int LIMBS = Fmt<DT>::LIMBS;
     static constexpr int CW = K * LIMBS;
     static constexpr int CWB = (K + XB) * LIMBS;
-    __host__ __device__ static int gq(int G, int nh = 0) { return (G + 1 + 32 * nh + 3) & ~3; }
+    __host__ __device__ static int gq(int G, int nh = 0) { return (G + TAB_SINKS + 32 * nh + 3) & ~3; }
     __host__ __device__ static int gr(int G) { return (G + 1 + 3) & ~3; }
     __host__ __device__ static size_t bytes(int G, int nh = 0) {
         return (size_t)gq(G, nh) * 4 * CWB + (size_t)gr(G) * 12 + (nh ? (size_t)G + 4 * TAB_HMAX : 0);
@@ -157,7 +160,7 @@ struct TabGeom {
 // GQC > 0: the counter-row stride is the compile-time constant GQC (>= gq(G)),
 // so every atomic's counter offset is an immediate.
 // HH: up to TAB_HMAX HEAVY groups (skewed keys, e.g. Zipf's head) get one
-// counter copy per lane in streaming mode -- virtual group G + 1 + 32 h +
+// counter copy per lane in streaming mode -- virtual group G + TAB_SINKS + 32 h +
 // lane, always bank = lane -- because many lanes of a warp adding to one
 // shared word serialise.  The copies are summed when published.
 // XB = 1: BAND MODE for blocks whose groups do not share one window top
@@ -251,7 +254,7 @@ struct Table {
     }
     // real group of a (virtual) group of the counter table
     __device__ __forceinline__ int real_group(int vg) const {
-        return (HH && vg > G) ? hkey[(vg - G - 1) >> 5] : vg;
+        return (HH && vg >= G + TAB_SINKS) ? hkey[(vg - G - TAB_SINKS) >> 5] : vg;
     }
     __device__ __forceinline__ void drain(int vg, int w, int kt) {
         const uint32_t c = atom_exch_shared(cbase + 4u * (uint32_t)vg + (uint32_t)w * wstride, 0u);
@@ -308,11 +311,11 @@ struct Table {
             const bool iu = (in >> u) & 1u;
             const bool ok = iu && (uint32_t)k < (uint32_t)G && hw < lim;
             exc |= (iu && !ok) ? 1u << u : 0u;
-            key[u] = ok ? k : G;  // sink group
+            key[u] = ok ? k : G + (int)(threadIdx.x & 31);  // this lane's sink
             val[u] = ok ? v : V(0);
             if (HH && nh > 0 && ok) {  // a heavy group's row goes to this lane's copy
                 const int hh = hmap[k];
-                if (hh >= 0) key[u] = G + 1 + 32 * hh + (int)(threadIdx.x & 31);
+                if (hh >= 0) key[u] = G + TAB_SINKS + 32 * hh + (int)(threadIdx.x & 31);
             }
         }
         uint32_t lo[4][K], hi[4][K], a[4];
@@ -369,7 +372,7 @@ struct Table {
         if (big & TAB_DRAIN_MASK) {  // rare: drain every counter of this batch that is past 2^29
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                if (key[u] == G) continue;  // the sink
+                if ((uint32_t)(key[u] - G) < (uint32_t)TAB_SINKS) continue;  // a sink
 #pragma unroll
                 for (int w = 0; w < CW; ++w) {
                     const uint32_t c = ld_shared_u32(a[u] + (uint32_t)w * wstride);
@@ -404,7 +407,7 @@ struct Table {
             const bool ok = iu && (uint32_t)k < (uint32_t)G && hw < lim && hw >= llim;
             exc |= (iu && !ok) ? 1u << u : 0u;
             const uint32_t s_ = hw < mlim ? 1u : 0u;
-            key[u] = ok ? k : G;  // sink group
+            key[u] = ok ? k : G + (int)(threadIdx.x & 31);  // this lane's sink
             val[u] = ok ? v : V(0);
             sh[u] = ok ? s_ : 0u;
             if (ok) {
@@ -415,7 +418,7 @@ struct Table {
                 }
                 if (HH && nh > 0) {
                     const int hh = hmap[k];
-                    if (hh >= 0) key[u] = G + 1 + 32 * hh + (int)(threadIdx.x & 31);
+                    if (hh >= 0) key[u] = G + TAB_SINKS + 32 * hh + (int)(threadIdx.x & 31);
                 }
             }
         }
@@ -470,7 +473,7 @@ struct Table {
         if (big & TAB_DRAIN_MASK) {  // rare: drain every counter of this batch's groups that is past 2^29
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                if (key[u] == G) continue;  // the sink
+                if ((uint32_t)(key[u] - G) < (uint32_t)TAB_SINKS) continue;  // a sink
                 const uint32_t g0 = cbase + 4u * (uint32_t)key[u];
 #pragma unroll
                 for (int w = 0; w < CWB; ++w) {
@@ -640,7 +643,7 @@ struct Table {
             for (int i = threadIdx.x; i < nh * CWB; i += TPB) {
                 const int h = i / CWB, w = i - h * CWB;
                 int64_t T = 0;
-                uint32_t *p = cnt + (size_t)w * gq + G + 1 + 32 * h;
+                uint32_t *p = cnt + (size_t)w * gq + G + TAB_SINKS + 32 * h;
                 for (int l = 0; l < 32; ++l) {
                     T += counter_part<DT>(w, p[l]);
                     p[l] = 0;
