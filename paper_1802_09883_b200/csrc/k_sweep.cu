@@ -112,11 +112,11 @@ SwPlan sw_plan(int64_t n, int32_t G) {
 // scatter stage: the tile's rows + every partition's carried rows (< SW_RUN
 // each), in partition order
 constexpr int SW_STAGE = SW_CTILE + (SW_RUN - 1) * SW_PMAX;
-template <int DT>
+template <int DT, typename DstT>
 size_t sw_smem_cold() {
     using V = typename Fmt<DT>::V;
-    return (size_t)SW_STAGE * (4 + sizeof(V) + 2) + (size_t)SW_PMAX * SW_RUN * (4 + sizeof(V)) +
-           (size_t)SW_PMAX * (8 + 6 * 4 + 8);
+    return (size_t)SW_STAGE * (4 + sizeof(V) + sizeof(DstT)) + (size_t)SW_PMAX * SW_RUN * (4 + sizeof(V)) +
+           (size_t)SW_PMAX * (8 + 4 * 4);
 }
 
 struct SwWs {
@@ -440,14 +440,18 @@ k_sw_scan(int64_t *__restrict__ cnt, int nb, int P, int64_t *__restrict__ pstart
 }
 
 // 5. the scatter of the cold rows.  Per tile: rank the rows by partition
-// (shared atomics), stage them in partition order behind the rows each
-// partition carried over from the previous tile, and write every
-// partition's whole run units (SW_RUN rows: full 32-byte sectors of keys and
-// of values) to the block's running position in that partition; the < SW_RUN
-// rows left over are carried to the next tile.  The block's last units are
-// padded with SW_PAD rows.  Every write is a whole, aligned sector, so DRAM
-// never has to merge partial sectors.
-template <int DT>
+// (shared atomics); each partition's rows -- the < SW_RUN rows it carried over
+// from the previous tile first, then the tile's -- are numbered j = 0 .. T-1;
+// rows j < F (F = T rounded down to whole run units of SW_RUN rows: full
+// 32-byte sectors of keys and values) are staged, in partition order, with
+// their destination (the block's running position in the partition + j), the
+// others are carried to the next tile.  The write phase then only reads
+// (key, value, destination) per staged row: consecutive threads write
+// consecutive rows of a run.  Runs of consecutive tiles abut, and every
+// write is a whole, aligned sector, so DRAM never merges partial sectors.  The
+// block's last units are padded with SW_PAD rows.  Destinations are DstT:
+// 32-bit unless the partitioned buffer holds 2^32 rows or more.
+template <int DT, typename DstT>
 __global__ void __launch_bounds__(SW_STPB, sw_cbps<DT>())
 k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals, int64_t n,
              const int32_t *__restrict__ bkeys, const typename Fmt<DT>::V *__restrict__ bvals, int32_t G, int gbits,
@@ -458,6 +462,7 @@ k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__rest
     static_assert(TPB >= SW_PMAX, "one thread per partition");
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_wsum[NW];
+    __shared__ int s_nw;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int Gp = 1 << gbits;
     if (ctrl[3] >= 0) { keys = bkeys; vals = bvals; }
@@ -465,21 +470,17 @@ k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__rest
     cold_range(ctrl, cs, n, blockIdx.x, gridDim.x, row0, row1);
     if (row0 >= row1) return;
     // shared memory: stage values | carried values | run | stage keys |
-    // carried keys | counts | offsets | carried counts | flushed counts |
-    // new-row offsets | stage partitions
+    // stage destinations | carried keys | per-partition counts
     V *tvals = reinterpret_cast<V *>(smem);
     V *cvals = tvals + SW_STAGE;
     int64_t *run = reinterpret_cast<int64_t *>(cvals + SW_PMAX * SW_RUN);  // next destination row per partition
-    int32_t *tkeys = reinterpret_cast<int32_t *>(run + SW_PMAX);
+    DstT *tdst = reinterpret_cast<DstT *>(run + SW_PMAX);
+    int32_t *tkeys = reinterpret_cast<int32_t *>(tdst + SW_STAGE);
     int32_t *ckeys = tkeys + SW_STAGE;
-    int32_t *tcnt = ckeys + SW_PMAX * SW_RUN;
-    int32_t *off = tcnt + SW_PMAX;
-    int32_t *ccnt = off + SW_PMAX;
-    int32_t *fl = ccnt + SW_PMAX;
-    int32_t *nb_ = fl + SW_PMAX;
-    int32_t *lim = nb_ + SW_PMAX;
-    int64_t *dbase = reinterpret_cast<int64_t *>(lim + SW_PMAX);  // (8-byte aligned: 7 int32 arrays of 256 after 8-byte data)
-    uint16_t *tpart = reinterpret_cast<uint16_t *>(dbase + SW_PMAX);
+    int32_t *tcnt = ckeys + SW_PMAX * SW_RUN;  // new rows of the tile
+    int32_t *ccnt = tcnt + SW_PMAX;            // rows carried into the tile
+    int32_t *fl = ccnt + SW_PMAX;              // rows written this tile (whole units)
+    int32_t *wof = fl + SW_PMAX;               // first stage slot of the partition's written rows
     for (int p = tid; p < P; p += TPB) {
         run[p] = base[(size_t)blockIdx.x * P + p];
         tcnt[p] = 0;
@@ -501,10 +502,11 @@ k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__rest
                 }
             }
         __syncthreads();  // B1: ranks complete
-        {  // per partition (thread p): carried + new rows -> stage offset, whole units to write
+        {  // per partition (thread p): whole units written this tile, their stage offset
             const int p = tid;
             const int T = p < P ? ccnt[p] + tcnt[p] : 0;
-            int incl = T;
+            const int F = T & ~(SW_RUN - 1);
+            int incl = F;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -515,56 +517,56 @@ k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__rest
             int b0 = 0;
             for (int w = 0; w < warp; ++w) b0 += s_wsum[w];
             if (p < P) {
-                const int o = b0 + incl - T;
-                off[p] = o;
-                nb_[p] = o + ccnt[p];  // the tile's new rows follow the carried ones
-                fl[p] = T & ~(SW_RUN - 1);
-                lim[p] = o + (T & ~(SW_RUN - 1));  // stage rows below lim[p] are written
-                dbase[p] = run[p] - o;             // destination of stage row s: dbase[p] + s
+                fl[p] = F;
+                wof[p] = b0 + incl - F;
             }
+            if (tid == TPB - 1) s_nw = b0 + incl;
         }
         __syncthreads();  // B2
-        for (int i = tid; i < P * SW_RUN; i += TPB) {  // carried rows first
+        // rows carried from the previous tile (numbers j < ccnt): staged when
+        // j < F; otherwise (F == 0) they stay where they are
+        for (int i = tid; i < P * SW_RUN; i += TPB) {
             const int p = i / SW_RUN, j = i % SW_RUN;
-            if (j < ccnt[p]) {
-                const int s_ = off[p] + j;
+            if (j < ccnt[p] && j < fl[p]) {
+                const int s_ = wof[p] + j;
                 tkeys[s_] = ckeys[i];
                 tvals[s_] = cvals[i];
-                tpart[s_] = (uint16_t)p;
+                tdst[s_] = (DstT)(run[p] + j);
             }
         }
+        __syncthreads();  // B2': the carried rows are read before new ones take their slots
 #pragma unroll
         for (int i = 0; i < QPT; ++i)
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                if (pp[i][u] < 0) continue;
-                const int s_ = nb_[pp[i][u]] + rk[i][u];
-                tkeys[s_] = kq(q[i].k, u) & (Gp - 1);
-                tvals[s_] = q[i].v(u);
-                tpart[s_] = (uint16_t)pp[i][u];
+                const int p = pp[i][u];
+                if (p < 0) continue;
+                const int j = ccnt[p] + rk[i][u];
+                const int f = fl[p];
+                if (j < f) {
+                    const int s_ = wof[p] + j;
+                    tkeys[s_] = kq(q[i].k, u) & (Gp - 1);
+                    tvals[s_] = q[i].v(u);
+                    tdst[s_] = (DstT)(run[p] + j);
+                } else {
+                    ckeys[p * SW_RUN + (j - f)] = kq(q[i].k, u) & (Gp - 1);
+                    cvals[p * SW_RUN + (j - f)] = q[i].v(u);
+                }
             }
-        __syncthreads();  // B3: stage complete, in partition order
-        const int ns = off[P - 1] + ccnt[P - 1] + tcnt[P - 1];
-        for (int s_ = tid; s_ < ns; s_ += TPB) {  // consecutive threads: consecutive rows of a run
-            const int p = tpart[s_];
-            const int l = lim[p];
-            if (s_ < l) {
-                const int64_t d = dbase[p] + s_;
-                pkeys[d] = tkeys[s_];
-                pvals[d] = tvals[s_];
-            } else {
-                ckeys[p * SW_RUN + (s_ - l)] = tkeys[s_];
-                cvals[p * SW_RUN + (s_ - l)] = tvals[s_];
-            }
+        __syncthreads();  // B3: stage complete
+        const int nw = s_nw;
+        for (int s_ = tid; s_ < nw; s_ += TPB) {  // consecutive threads: consecutive rows of a run
+            const DstT d = tdst[s_];
+            pkeys[d] = tkeys[s_];
+            pvals[d] = tvals[s_];
         }
-        __syncthreads();  // B4: the stage is read
         for (int p = tid; p < P; p += TPB) {
             const int T = ccnt[p] + tcnt[p];
             run[p] += fl[p];
             ccnt[p] = T - fl[p];
             tcnt[p] = 0;
         }
-        __syncthreads();  // B5: counts reset before the next tile's ranks
+        __syncthreads();  // B4: the stage is read and the counts reset before the next tile's ranks
     };
 
     const int64_t nq = (row1 - row0) >> 2;
@@ -677,13 +679,14 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
     if (rr != -1) return rr;
     const SwPlan pl = sw_plan<DT, K>(n, G);
     if (pl.P > SW_PMAX) return -1;
-    const size_t sm_cold = sw_smem_cold<DT>();
+    const bool d32 = pl.rows_cap < ((int64_t)1 << 32);  // 32-bit scatter destinations
+    const size_t sm_cold = d32 ? sw_smem_cold<DT, uint32_t>() : sw_smem_cold<DT, unsigned long long>();
     const size_t sm_tab = TabGeom<DT, K, 1>::bytes(pl.Gp);  // accumulate
     const size_t sm_hot = TabGeom<DT, K, 1>::bytes(pl.Gp, TAB_HMAX);  // hot pass (+ heavy-group lane copies)
     if (sm_hot > (size_t)device_props().smem_optin - 1024) return -1;
     SwWs w = sw_carve<DT, K>(ws, n, G, pl);
     if (w.bytes > ws_bytes) return -1;
-    static thread_local size_t conf_h = 0, conf_c = 0, conf_a = 0;
+    static thread_local size_t conf_h = 0, conf_c = 0, conf_c64 = 0, conf_a = 0;
     auto conf = [](auto kern, size_t &have, size_t want) {
         if (have >= want) return true;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want) != cudaSuccess)
@@ -691,7 +694,7 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
         have = want;
         return true;
     };
-    if (!conf(k_sweep_hot<DT, K>, conf_h, sm_hot) || !conf(k_sweep_cold<DT>, conf_c, sm_cold) ||
+    if (!conf(k_sweep_hot<DT, K>, conf_h, sm_hot) || !(d32 ? conf(k_sweep_cold<DT, uint32_t>, conf_c, sm_cold) : conf(k_sweep_cold<DT, unsigned long long>, conf_c64, sm_cold)) ||
         !conf(k_sweep_acc<DT, K>, conf_a, sm_tab))
         return -2;
     if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return -2;
@@ -719,9 +722,14 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
         });
         if (rc) return rc;
         rc = traced("sweep_scatter", st, launches, [&] {
-            k_sweep_cold<DT><<<pl.cgrid, SW_STPB, sm_cold, st>>>(keys, (const V *)vals, n, w.bkeys,
-                                                                 (const V *)w.bvals, G, pl.gbits, pl.P, w.cnt,
-                                                                 w.pkeys, (V *)w.pvals, w.ctrl, cs);
+            if (d32)
+                k_sweep_cold<DT, uint32_t><<<pl.cgrid, SW_STPB, sm_cold, st>>>(
+                    keys, (const V *)vals, n, w.bkeys, (const V *)w.bvals, G, pl.gbits, pl.P, w.cnt, w.pkeys,
+                    (V *)w.pvals, w.ctrl, cs);
+            else
+                k_sweep_cold<DT, unsigned long long><<<pl.cgrid, SW_STPB, sm_cold, st>>>(
+                    keys, (const V *)vals, n, w.bkeys, (const V *)w.bvals, G, pl.gbits, pl.P, w.cnt, w.pkeys,
+                    (V *)w.pvals, w.ctrl, cs);
         });
         if (rc) return rc;
         rc = traced("sweep_accumulate", st, launches, [&] {
