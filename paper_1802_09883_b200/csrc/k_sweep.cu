@@ -51,6 +51,9 @@ constexpr int SW_HTPB = 512;           // hot-partition pass (one block per SM: 
 #ifndef SW_HU
 #define SW_HU 16      // 16-byte key vectors in flight per histogram thread (4: 0.29 ms, 8: 0.24, 16: 0.21 at 2^28 keys)
 #endif
+#ifndef SW_HQ
+#define SW_HQ 1       // hot pass: quads per thread per step (issue-bound: 2 and 4 measured slower)
+#endif
 #ifndef SW_L2PF
 #define SW_L2PF 0     // scatter / accumulate: lane 0 of each warp bulk-prefetches its rows two steps ahead into L2
 #endif
@@ -328,15 +331,27 @@ k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restr
         tab.quad(hq, hin, flags);
     };
     const int64_t nq = (row1 - row0) >> 2;
-    const int64_t steps = (nq + SW_HTPB - 1) / SW_HTPB;
-    QuadT<DT> nxt;
+    // QH quads per thread per step, the next step's in flight (memory-level
+    // parallelism: one block of 512 threads per SM holds the table)
+    constexpr int QH = SW_HQ;
+    const int64_t steps = (nq + SW_HTPB * QH - 1) / (SW_HTPB * QH);
+    QuadT<DT> nxt[QH];
     const bool vec = ((((uintptr_t)keys) | ((uintptr_t)vals)) & 15) == 0;  // (rows r0 are quad multiples)
-    if (tid < nq) load_quad_rt<DT>(keys, vals, row0 + 4 * (int64_t)tid, nxt, vec);
+#pragma unroll
+    for (int i = 0; i < QH; ++i)
+        if (i * SW_HTPB + tid < nq) load_quad_rt<DT>(keys, vals, row0 + 4 * (int64_t)(i * SW_HTPB + tid), nxt[i], vec);
     for (int64_t s = 0; s < steps; ++s) {
-        const QuadT<DT> q = nxt;
-        const int64_t qi = s * SW_HTPB + tid;
-        if (qi + SW_HTPB < nq) load_quad_rt<DT>(keys, vals, row0 + 4 * (qi + SW_HTPB), nxt, vec);
-        step(q, qi < nq ? 0xFu : 0u);
+        QuadT<DT> cur[QH];
+#pragma unroll
+        for (int i = 0; i < QH; ++i) cur[i] = nxt[i];
+        const int64_t q0 = s * SW_HTPB * QH + tid;
+#pragma unroll
+        for (int i = 0; i < QH; ++i) {
+            const int64_t qn = q0 + (int64_t)(QH + i) * SW_HTPB;
+            if (qn < nq) load_quad_rt<DT>(keys, vals, row0 + 4 * qn, nxt[i], vec);
+        }
+#pragma unroll
+        for (int i = 0; i < QH; ++i) step(cur[i], q0 + (int64_t)i * SW_HTPB < nq ? 0xFu : 0u);
     }
     const int tail = (int)(row1 - row0 - 4 * nq);
     if (tail > 0) {

@@ -1,0 +1,11 @@
+#!/bin/bash
+# k_lean_multi: L2 bulk prefetch of the rows a few steps ahead (config 4, config 2 at G=16)
+cd $GRAFT_REPO_ROOT
+B="python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-atomic-baseline --no-configs --no-e2e --no-parity"
+for v in main lpf2 lpf4; do
+  L=""; [ $v != main ] && L="REPRO_B200_LIB=$PWD/scripts/variants/lib_$v.so"
+  for c in "--config 4" "--config 2 --n-groups 16"; do
+    env $L timeout 600 $B $c > /tmp/b.json 2>/tmp/b.err
+    python -c "import json; d=json.load(open('/tmp/b.json')); print('$v $c', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['per_kernel_ms'].items()})" || tail -3 /tmp/b.err
+  done
+done
