@@ -946,6 +946,10 @@ int launch_route_xb(const int32_t *keys, const void *vals, int64_t n, int32_t G,
                                                           args, pl.smem, st);
         ++*launches;
         trace_end(tok, "route", st);
+        if (e == cudaErrorCooperativeLaunchTooLarge) {  // not every SM free (e.g. a concurrent stream):
+            (void)cudaGetLastError();                    // the sweep runs instead (it re-zeroes its own workspace)
+            return -1;
+        }
         if (e != cudaSuccess) return -2;
     }
     if (!out && !acc_k) return 0;  // deposit only (the split form reads the slot table)

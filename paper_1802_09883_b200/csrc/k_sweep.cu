@@ -805,7 +805,8 @@ size_t sweep_workspace_bytes(int64_t n, int32_t G, int K, int DT) {
 #define SWB(dt, k)                                          \
     if (DT == dt && K == k) {                               \
         const SwPlan pl = sw_plan<dt, k>(n, G);             \
-        return std::max(sw_carve<dt, k>(nullptr, n, G, pl).bytes, route_workspace_bytes(G, k, dt)); \
+        return std::max(sw_carve<dt, k>(nullptr, n, G, pl).bytes,                                   \
+                        route_mode() ? route_workspace_bytes(G, k, dt) : (size_t)0); /* (rings: opt-in) */ \
     }
     SWB(1, 1) SWB(1, 2) SWB(1, 3) SWB(1, 4) SWB(0, 1) SWB(0, 2) SWB(0, 3) SWB(0, 4)
 #undef SWB
