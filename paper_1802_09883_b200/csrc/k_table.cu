@@ -55,7 +55,10 @@ namespace {
 #define TAB_QPT 2  // quads (4 rows) per thread per step (256-thread kernels); the next step's are in flight
 #endif
 #ifndef TAB_QPT512
-#define TAB_QPT512 1  // the same for the 512-thread (> 2048 groups) kernels
+#define TAB_QPT512 1  // the same for the one-block-per-SM (> 2048 groups) kernels
+#endif
+#ifndef TAB_BIGTPB
+#define TAB_BIGTPB 512  // threads of the one-block-per-SM (> 2048 groups) kernels (384, with 1 or 2 quads: slower)
 #endif
 #ifndef TAB_L2PF
 #define TAB_L2PF 0  // (measured slower: 0.419 -> 0.461 ms at 3 steps) steps ahead whose rows lane 0 of each warp prefetches into L2 (0: off)
@@ -201,8 +204,8 @@ int launch_table_any(int DT, int K, const int32_t *keys, const void *vals, int64
         return G <= 1024 ? launch_table_t<dt, k, 256, 1056, 0>(keys, vals, n, G, kglob, slots, status, st, launches) \
              : G <= 2048 ? launch_table_t<dt, k, 256, 0, 0>(keys, vals, n, G, kglob, slots, status, st, launches)    \
              : TabGeom<dt, k, 1>::bytes(G) <= (size_t)device_props().smem_optin - 1024                              \
-                         ? launch_table_t<dt, k, 512, 0, 1>(keys, vals, n, G, kglob, slots, status, st, launches)   \
-                         : launch_table_t<dt, k, 512, 0, 0>(keys, vals, n, G, kglob, slots, status, st, launches);
+                         ? launch_table_t<dt, k, TAB_BIGTPB, 0, 1>(keys, vals, n, G, kglob, slots, status, st, launches)   \
+                         : launch_table_t<dt, k, TAB_BIGTPB, 0, 0>(keys, vals, n, G, kglob, slots, status, st, launches);
     TAB_CASE(1, 1) TAB_CASE(1, 2) TAB_CASE(1, 3) TAB_CASE(1, 4)
     TAB_CASE(0, 1) TAB_CASE(0, 2) TAB_CASE(0, 3) TAB_CASE(0, 4)
 #undef TAB_CASE
