@@ -542,11 +542,12 @@ def run_workload(R, torch, args, config, n, G, K, dts, world, rank, local, steps
         res["rejected"] = f"device status {st_a or st_b} during the timed steps"
 
     # non-reproducible atomicAdd GroupBy on the same GPU and the same rows:
-    # the fastest of the four variants (global RED per row, shared-memory
-    # table, register partials for <= 16 groups, warp aggregation of equal keys)
+    # the fastest of the five variants (global RED per row, shared-memory
+    # table, register partials for <= 16 groups, warp aggregation of equal
+    # keys, heavy hitters privatised per block)
     if atomic and world == 1 and not multi and not array:
         best = None
-        for variant in (0, 1, 2, 3):
+        for variant in (0, 1, 2, 3, 4):
             try:
                 for _ in range(3):
                     R.baseline_atomic_sum(keys, cols[0], G, variant=variant, stream=stream)
@@ -565,7 +566,7 @@ def run_workload(R, torch, args, config, n, G, K, dts, world, rank, local, steps
                 continue
         if best:
             names = ["global_atomicAdd", "smem_privatised_atomicAdd", "register_partials_atomicAdd",
-                     "warp_aggregated_atomicAdd"]
+                     "warp_aggregated_atomicAdd", "heavy_hitters_privatised_atomicAdd"]
             res["baseline_atomic"] = {"variant": names[best[0]], "ms_per_step": best[1],
                                       "rows_per_s": n / (best[1] * 1e-3),
                                       "slowdown_repro_vs_atomic": ms_per_step / best[1]}

@@ -431,7 +431,10 @@ int repro_acc_window_import_range(repro_acc *acc, int32_t g0, int32_t count,
  * and-swap on sm_100a) flushed with global atomics; variant 2 (n_groups <=
  * 16): per-thread register partials, one global atomic per group per warp;
  * variant 3: warp aggregation of equal keys (match.any), one global atomic
- * per distinct key per warp.  out is zeroed inside.  Stream-ordered,
+ * per distinct key per warp; variant 4: heavy hitters privatised (the keys
+ * holding >= 1/2048 of 8192 sampled rows, at most 256, summed per warp in
+ * shared memory and flushed once per block; the other rows by global
+ * atomicAdd).  out is zeroed inside.  Stream-ordered,
  * non-blocking; returns REPRO_EINVAL for bad arguments or when the variant
  * does not apply (1: shared memory too small, 2: n_groups > 16).
  * ---------------------------------------------------------------------- */

@@ -1368,9 +1368,9 @@ int repro_baseline_atomic_sum(const int32_t *keys, const void *vals, int64_t n, 
     if (n < 0 || n_groups < 1 || (dtype != 0 && dtype != 1) || !out || (n > 0 && (!keys || !vals)))
         return REPRO_EINVAL;
     cudaStream_t st = (cudaStream_t)stream;
-    static const char *names[4] = {"baseline_atomic_global", "baseline_atomic_smem", "baseline_atomic_regs",
-                                   "baseline_atomic_match"};
-    if (variant < 0 || variant > 3) return REPRO_EINVAL;
+    static const char *names[5] = {"baseline_atomic_global", "baseline_atomic_smem", "baseline_atomic_regs",
+                                   "baseline_atomic_match", "baseline_atomic_heavy"};
+    if (variant < 0 || variant > 4) return REPRO_EINVAL;
     return map_launch(timed(names[variant], st, [&] {
         return launch_baseline(dtype, variant, accumulate_f64, keys, vals, n, n_groups, out, st, &t_launches);
     }));

@@ -411,9 +411,33 @@ def test_atomic_baseline_is_not_reproducible(R):
 def test_atomic_baseline_close_to_repro(R):
     keys, vals = synth.generate_chunked(1, 1 << 20, 1024)
     rep = gpu_groupby(R, keys, vals, 1024, 3)
-    for variant in (0, 1):
+    for variant in (0, 1, 3, 4):
         b = R.baseline_atomic_sum(dev(keys), dev(vals), 1024, variant=variant).cpu().numpy()
         np.testing.assert_allclose(b, rep, rtol=1e-9, atol=1e-6)
+
+
+@pytest.mark.parametrize("n", [(1 << 20) + 3, 1001, 5])
+def test_atomic_baseline_register_variant(R, n):
+    # G <= 16: 16-byte loads with a scalar remainder (ragged n)
+    rng = np.random.default_rng(n)
+    keys = rng.integers(0, 16, n, dtype=np.int32)
+    vals = rng.uniform(-1, 1, n)
+    rep = gpu_groupby(R, keys, vals, 16, 3)
+    b = R.baseline_atomic_sum(dev(keys), dev(vals), 16, variant=2).cpu().numpy()
+    np.testing.assert_allclose(b, rep, rtol=1e-9, atol=1e-9)
+
+
+def test_atomic_baseline_heavy_hitters_on_zipf(R):
+    # skewed keys: the heavy keys are summed per warp in shared memory, the
+    # rest by global atomics; the sums agree with the reproducible ones
+    rng = np.random.default_rng(7)
+    G, n = 1 << 18, (1 << 21) + 1
+    p = np.arange(1, G + 1, dtype=np.float64) ** -1.1
+    keys = np.minimum(np.searchsorted(np.cumsum(p / p.sum()), rng.random(n)), G - 1).astype(np.int32)
+    vals = rng.uniform(-1, 1, n)
+    rep = gpu_groupby(R, keys, vals, G, 3)
+    b = R.baseline_atomic_sum(dev(keys), dev(vals), G, variant=4).cpu().numpy()
+    np.testing.assert_allclose(b, rep, rtol=1e-9, atol=1e-9)
 
 
 # ------------------------------------------------- partitioned path (row a5)
