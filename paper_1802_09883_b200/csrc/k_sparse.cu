@@ -6,17 +6,16 @@
 //   1. k_hash_insert   open addressing (linear probing, 64-bit CAS) of every
 //                      row's key into a table of 2^b slots
 //   2. k_hash_collect  the distinct keys (in table order)
-//   3. sort            the distinct keys ascending (cub radix sort): the dense
-//                      id of a key is its rank, so ids -- and the output
-//                      order -- depend only on the SET of keys
+//   3. sort            the distinct keys ascending (LSD radix sort of the
+//                      64-bit slot words, 8 passes of 8-bit digits: k_rs_*):
+//                      the dense id of a key is its rank, so ids -- and the
+//                      output order -- depend only on the SET of keys
 //   4. k_hash_assign   rank -> the key's slot
 //   5. k_hash_map      every row's id
 // The sums are the dense path's, so the result bits depend only on the
 // multiset of (key, value) pairs.  Slots hold key ^ 2^63 (0 = empty, so the
 // table is cleared with a memset); the key INT64_MIN is reserved (EKEY).
 #include <algorithm>
-
-#include <cub/device/device_radix_sort.cuh>
 
 #include "common.cuh"
 #include "internal.h"
@@ -71,10 +70,11 @@ __global__ void k_hash_insert(const KeyT *__restrict__ keys, int64_t n, unsigned
     if (bad) atomicOr(status, bad);
 }
 
-__global__ void k_hash_collect(const unsigned long long *tk, uint64_t cap, int64_t *out, unsigned long long *count) {
+__global__ void k_hash_collect(const unsigned long long *tk, uint64_t cap, unsigned long long *out,
+                               unsigned long long *count) {
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cap; i += (uint64_t)gridDim.x * blockDim.x) {
         const unsigned long long s = tk[i];
-        if (s != 0ull) out[atomicAdd(count, 1ull)] = (int64_t)(s ^ FLIP);
+        if (s != 0ull) out[atomicAdd(count, 1ull)] = s;  // (slot word: unsigned order = key order)
     }
 }
 
@@ -84,10 +84,94 @@ __device__ __forceinline__ uint64_t find_slot(const unsigned long long *tk, uint
     return h;
 }
 
-__global__ void k_hash_assign(const int64_t *__restrict__ sorted, int64_t d, const unsigned long long *tk,
-                              uint64_t mask, int32_t *tid) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x)
-        tid[find_slot(tk, mask, (unsigned long long)sorted[i] ^ FLIP)] = (int32_t)i;
+__global__ void k_hash_assign(const unsigned long long *__restrict__ sorted, int64_t d, const unsigned long long *tk,
+                              uint64_t mask, int32_t *tid, int64_t *keys_out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long s = sorted[i];
+        tid[find_slot(tk, mask, s)] = (int32_t)i;
+        keys_out[i] = (int64_t)(s ^ FLIP);
+    }
+}
+
+// LSD radix sort of d distinct 64-bit words, 8-bit digits: per pass a tile
+// histogram, then a stable scatter that derives its own offsets from all the
+// tiles' histograms (digit base + the counts of the earlier tiles).  Tiles of
+// RS_TILE words; the scatter ranks a tile in 8 rounds of 256 consecutive
+// words (warp match -> rank among equal digits, per-warp counts -> prefix
+// over the warps), so equal digits keep their order.
+constexpr int RS_TPB = 256, RS_ROUNDS = 8, RS_TILE = RS_TPB * RS_ROUNDS;
+
+__global__ void __launch_bounds__(RS_TPB)
+k_rs_hist(const unsigned long long *__restrict__ in, int64_t d, int shift, uint32_t *__restrict__ hist) {
+    __shared__ uint32_t h[256];
+    const int tid = threadIdx.x;
+    h[tid] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+    for (int i = tid; i < RS_TILE; i += RS_TPB)
+        if (base + i < d) atomicAdd(&h[(unsigned)(in[base + i] >> shift) & 255u], 1u);
+    __syncthreads();
+    hist[(size_t)blockIdx.x * 256 + tid] = h[tid];  // tile-major
+}
+
+__global__ void __launch_bounds__(RS_TPB)
+k_rs_scatter(const unsigned long long *__restrict__ in, unsigned long long *__restrict__ out, int64_t d, int shift,
+             const uint32_t *__restrict__ hist, int nt) {
+    __shared__ uint32_t wcnt[RS_TPB / 32][256];
+    __shared__ uint32_t run[256];
+    __shared__ uint32_t wsum[RS_TPB / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t base = (int64_t)blockIdx.x * RS_TILE;
+    unsigned long long x[RS_ROUNDS];  // the tile's words, loaded up front
+#pragma unroll
+    for (int r = 0; r < RS_ROUNDS; ++r) {
+        const int64_t i = base + r * RS_TPB + tid;
+        x[r] = i < d ? in[i] : 0ull;
+    }
+    {  // thread = digit: words of this digit in earlier tiles, and in all tiles
+        uint32_t pre = 0, tot = 0;
+#pragma unroll 8
+        for (int t = 0; t < nt; ++t) {
+            const uint32_t c = hist[(size_t)t * 256 + tid];
+            pre += t < (int)blockIdx.x ? c : 0u;
+            tot += c;
+        }
+        uint32_t incl = tot;  // exclusive scan of the digit totals over the block
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        uint32_t wb = 0;
+        for (int w = 0; w < warp; ++w) wb += wsum[w];
+        run[tid] = wb + incl - tot + pre;
+    }
+    for (int r = 0; r < RS_ROUNDS; ++r) {
+#pragma unroll
+        for (int w = 0; w < RS_TPB / 32; ++w) wcnt[w][tid] = 0;
+        __syncthreads();
+        const bool ok = base + r * RS_TPB + tid < d;
+        const int dig = ok ? (int)((unsigned)(x[r] >> shift) & 255u) : 256;
+        const unsigned peers = __match_any_sync(0xffffffffu, dig);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        if (ok && rank == 0) wcnt[warp][dig] = __popc(peers);
+        __syncthreads();
+        {  // thread = digit: exclusive prefix over the warps of this round
+            uint32_t acc = run[tid];
+#pragma unroll
+            for (int w = 0; w < RS_TPB / 32; ++w) {
+                const uint32_t c = wcnt[w][tid];
+                wcnt[w][tid] = acc;
+                acc += c;
+            }
+            run[tid] = acc;
+        }
+        __syncthreads();
+        if (ok) out[wcnt[warp][dig] + rank] = x[r];
+        __syncthreads();
+    }
 }
 
 template <typename KeyT>
@@ -105,11 +189,11 @@ int grid_for(int64_t n) {
 
 size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
+int rs_tiles(int64_t items) { return (int)((std::max<int64_t>(items, 1) + RS_TILE - 1) / RS_TILE); }
+
+// radix sort scratch: the ping-pong buffer + the (tile, digit) counts
 size_t sort_tmp_bytes(int64_t items) {
-    size_t tmp = 0;
-    cub::DeviceRadixSort::SortKeys(nullptr, tmp, (const int64_t *)nullptr, (int64_t *)nullptr,
-                                   (int)std::max<int64_t>(items, 1));
-    return tmp;
+    return al256(8 * (size_t)std::max<int64_t>(items, 1)) + al256(4 * 256 * (size_t)rs_tiles(items));
 }
 
 }  // namespace
@@ -142,7 +226,7 @@ int sparse_map_keys(const KeyT *keys, int64_t n, int64_t max_groups, void *scrat
     p += al256(8 * cap);
     int32_t *tid = (int32_t *)p;
     p += al256(4 * cap);
-    int64_t *dk = (int64_t *)p;
+    unsigned long long *dk = (unsigned long long *)p;  // distinct slot words (sorted in place)
     p += al256(8 * mg);
     unsigned long long *cnt = (unsigned long long *)p;  // [0] distinct (insert), [1] collected
     p += al256(16);
@@ -165,10 +249,18 @@ int sparse_map_keys(const KeyT *keys, int64_t n, int64_t max_groups, void *scrat
     if (d > 0) {
         k_hash_collect<<<grid_for((int64_t)cap), 256, 0, st>>>(tk, cap, dk, cnt + 1);
         ++*launches;
-        size_t t = tmp;
-        if (cub::DeviceRadixSort::SortKeys(ctmp, t, dk, sorted_out, (int)d, 0, 64, st) != cudaSuccess) return -2;
-        ++*launches;
-        k_hash_assign<<<grid_for((int64_t)d), 256, 0, st>>>(sorted_out, (int64_t)d, tk, mask, tid);
+        (void)tmp;
+        unsigned long long *alt = (unsigned long long *)ctmp;
+        uint32_t *hist = (uint32_t *)((char *)ctmp + al256(8 * mg));
+        const int nt = rs_tiles((int64_t)d);
+        unsigned long long *src = dk, *dst = alt;
+        for (int shift = 0; shift < 64; shift += 8) {  // 8 passes: the words end in dk
+            k_rs_hist<<<nt, RS_TPB, 0, st>>>(src, (int64_t)d, shift, hist);
+            k_rs_scatter<<<nt, RS_TPB, 0, st>>>(src, dst, (int64_t)d, shift, hist, nt);
+            *launches += 2;
+            std::swap(src, dst);
+        }
+        k_hash_assign<<<grid_for((int64_t)d), 256, 0, st>>>(dk, (int64_t)d, tk, mask, tid, sorted_out);
         ++*launches;
         k_hash_map<<<grid_for(n), 256, 0, st>>>(keys, n, tk, mask, tid, ids);
         ++*launches;

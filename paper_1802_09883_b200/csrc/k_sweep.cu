@@ -60,6 +60,15 @@ constexpr int SW_HTPB = 512;           // hot-partition pass (one block per SM: 
 #ifndef SW_SQPT
 #define SW_SQPT 2     // quads per thread per scatter tile
 #endif
+#ifndef SW_BAL
+#define SW_BAL 1      // accumulate: equal row ranges per SM cut at partition bounds (0: 2^19-row items from a queue)
+#endif
+#ifndef SW_PUBROWS
+#define SW_PUBROWS 131072  // SW_BAL cost of one table clear + publish in rows (~60 us at G_p = 4096, binary64 K = 3)
+#endif
+#ifndef SW_MRANK
+#define SW_MRANK 8    // scatter ranks by warp match + one atomic per distinct partition up to this many partitions
+#endif                // (P = 4: 1.744 -> 1.542 ms; P = 16: 1.617 -> 1.743; P = 256: 2.30 -> 3.07 -- one atomic per row)
 #ifndef SW_CBPS64
 #define SW_CBPS64 2   // scatter blocks per SM, binary64 (shared memory: stage + carry)
 #endif
@@ -114,7 +123,7 @@ SwPlan sw_plan(int64_t n, int32_t G) {
     pl.cgrid = sw_cbps<DT>() * device_props().sms;
     // every (scatter block, partition) range is padded to whole run units
     pl.rows_cap = n + (int64_t)SW_RUN * pl.cgrid * pl.P + SW_RUN;
-    pl.max_items = pl.P + (pl.rows_cap + SW_IROWS - 1) / SW_IROWS + 1;
+    pl.max_items = SW_BAL ? pl.P + pl.grid + 1 : pl.P + (pl.rows_cap + SW_IROWS - 1) / SW_IROWS + 1;
     return pl;
 }
 
@@ -141,6 +150,7 @@ struct SwWs {
     int64_t *cnt;       // [cgrid][P] rows per (block, partition), then destination bases
     int64_t *pstart;    // [P + 1] first row of each partition
     int64_t *items;     // [max_items][3] partition, first row, end row
+    int32_t *bfirst;    // [grid + 1] first item of each accumulate block (SW_BAL)
     size_t bytes;
 };
 
@@ -167,6 +177,7 @@ SwWs sw_carve(void *ws, int64_t n, int32_t G, const SwPlan &pl) {
     w.cnt = (int64_t *)take(8 * (size_t)pl.cgrid * pl.P);
     w.pstart = (int64_t *)take(8 * ((size_t)pl.P + 1));
     w.items = (int64_t *)take(24 * (size_t)pl.max_items);
+    w.bfirst = (int32_t *)take(4 * ((size_t)pl.grid + 1));
     w.bytes = o;
     return w;
 }
@@ -417,9 +428,12 @@ __device__ __forceinline__ int64_t sw_pad(int64_t c) { return (c + SW_RUN - 1) &
 
 __global__ void __launch_bounds__(1024)
 k_sw_scan(int64_t *__restrict__ cnt, int nb, int P, int64_t *__restrict__ pstart, int32_t *__restrict__ pkeys,
-          int64_t *__restrict__ items, int32_t *__restrict__ ctrl) {
+          int64_t *__restrict__ items, int32_t *__restrict__ bfirst, int na, int32_t *__restrict__ ctrl) {
     __shared__ int64_t part[4][SW_PMAX];
     __shared__ int64_t start[SW_PMAX + 1];
+    __shared__ int64_t cps[SW_PMAX + 1];  // SW_BAL: cost before each partition
+    __shared__ int64_t cuts[1025];        // SW_BAL: first row of each accumulate block (na <= 1024)
+    __shared__ int32_t nitm[1025];
     const int tid = threadIdx.x;
     const int p = tid & (SW_PMAX - 1), quarter = tid >> 8;  // 4 threads per partition
     const int b0 = nb * quarter / 4, b1 = nb * (quarter + 1) / 4;
@@ -431,20 +445,96 @@ k_sw_scan(int64_t *__restrict__ cnt, int nb, int P, int64_t *__restrict__ pstart
     }
     __syncthreads();
     if (tid == 0) {
-        int64_t a = 0, it = 0;
+        int64_t a = 0, it = 0, c = 0;
         for (int q = 0; q < P; ++q) {
             const int64_t tot = part[0][q] + part[1][q] + part[2][q] + part[3][q];
             start[q] = a;
-            for (int64_t r = 0; r < tot; r += SW_IROWS, ++it) {  // items of whole run units
-                items[3 * it] = q;
-                items[3 * it + 1] = a + r;
-                items[3 * it + 2] = a + min(tot, r + SW_IROWS);
-            }
+            cps[q] = c;
+            if (tot > 0) c += tot + SW_PUBROWS;
+            if (!SW_BAL)
+                for (int64_t r = 0; r < tot; r += SW_IROWS, ++it) {  // items of whole run units
+                    items[3 * it] = q;
+                    items[3 * it + 1] = a + r;
+                    items[3 * it + 2] = a + min(tot, r + SW_IROWS);
+                }
             a += tot;
         }
         start[P] = a;
-        ctrl[0] = (int32_t)it;
-        ctrl[1] = 0;
+        cps[P] = c;
+        if (!SW_BAL) {
+            ctrl[0] = (int32_t)it;
+            ctrl[1] = 0;
+        }
+    }
+    if (SW_BAL) {
+        // accumulate block b takes rows [cuts[b], cuts[b + 1]) of the
+        // partitioned buffer (cuts on whole run units), split where a
+        // partition ends (one table clear + publish per partition it
+        // touches).  The cuts are equal steps of a cost coordinate in which
+        // every non-empty partition costs its rows + SW_PUBROWS; a cut that
+        // lands in a partition's publish share snaps to the partition's start.
+        __syncthreads();
+        const int64_t a = start[P], ctot = cps[P];
+        if (tid <= na) {
+            int64_t ct = a;
+            if (tid < na) {
+                const int64_t x = ctot * tid / na;
+                if (x < ctot) {
+                    int lo = 0, hi = P;  // cps[lo] <= x < cps[hi]
+                    while (hi - lo > 1) {
+                        const int mid = (lo + hi) >> 1;
+                        if (cps[mid] <= x) lo = mid; else hi = mid;
+                    }
+                    const int64_t rq = start[lo + 1] - start[lo];
+                    ct = start[lo] + (min(rq, max((int64_t)0, x - cps[lo] - SW_PUBROWS)) & ~(int64_t)(SW_RUN - 1));
+                }
+            }
+            cuts[tid] = ct;
+        }
+        __syncthreads();
+        // the non-empty partitions of block tid's range: [qlo, qhi]
+        auto part_of = [&](int64_t r) {  // the last partition starting at or before row r (non-empty)
+            int lo = 0, hi = P;
+            while (hi - lo > 1) {
+                const int mid = (lo + hi) >> 1;
+                if (start[mid] <= r) lo = mid; else hi = mid;
+            }
+            return lo;
+        };
+        int qlo = 0, qhi = -1;
+        if (tid < na && cuts[tid] < cuts[tid + 1]) {
+            qlo = part_of(cuts[tid]);
+            qhi = part_of(cuts[tid + 1] - 1);
+        }
+        if (tid < na) {
+            int m = 0;
+            for (int q = qlo; q <= qhi; ++q) m += start[q + 1] > start[q];
+            nitm[tid] = m;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int t = 0;
+            for (int b = 0; b < na; ++b) {
+                const int m = nitm[b];
+                nitm[b] = t;
+                t += m;
+            }
+            nitm[na] = t;
+            ctrl[0] = t;
+            ctrl[1] = 0;
+        }
+        __syncthreads();
+        if (tid <= na) bfirst[tid] = nitm[tid];
+        if (tid < na) {
+            int it = nitm[tid];
+            for (int q = qlo; q <= qhi; ++q) {
+                if (start[q + 1] <= start[q]) continue;
+                items[3 * it] = q;
+                items[3 * it + 1] = max(cuts[tid], start[q]);
+                items[3 * it + 2] = min(cuts[tid + 1], start[q + 1]);
+                ++it;
+            }
+        }
     }
     __syncthreads();
     for (int q = tid; q <= P; q += 1024) pstart[q] = start[q];
@@ -472,7 +562,7 @@ k_sw_scan(int64_t *__restrict__ cnt, int nb, int P, int64_t *__restrict__ pstart
 // write is a whole, aligned sector, so DRAM never merges partial sectors.  The
 // block's last units are padded with SW_PAD rows.  Destinations are DstT:
 // 32-bit unless the partitioned buffer holds 2^32 rows or more.
-template <int DT, typename DstT>
+template <int DT, typename DstT, bool MR>
 __global__ void __launch_bounds__(SW_STPB, sw_cbps<DT>())
 k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals, int64_t n,
              const int32_t *__restrict__ bkeys, const typename Fmt<DT>::V *__restrict__ bvals, int32_t G, int gbits,
@@ -517,7 +607,17 @@ k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__rest
             for (int u = 0; u < 4; ++u) {
                 const int32_t k = kq(q[i].k, u);
                 pp[i][u] = -1;
-                if (((in[i] >> u) & 1u) && (uint32_t)k < (uint32_t)G) {
+                if (MR) {  // warp-aggregated: one shared atomic per distinct partition per warp (few partitions)
+                    const bool ok = ((in[i] >> u) & 1u) && (uint32_t)k < (uint32_t)G;
+                    const int pv = ok ? k >> gbits : -1;
+                    const unsigned peers = __match_any_sync(0xffffffffu, pv);
+                    const int leader = __ffs(peers) - 1;
+                    int b = 0;
+                    if (ok && lane == leader) b = atomicAdd(&tcnt[pv], __popc(peers));
+                    b = __shfl_sync(0xffffffffu, b, leader);
+                    pp[i][u] = pv;
+                    rk[i][u] = b + __popc(peers & ((1u << lane) - 1u));
+                } else if (((in[i] >> u) & 1u) && (uint32_t)k < (uint32_t)G) {
                     pp[i][u] = k >> gbits;
                     rk[i][u] = atomicAdd(&tcnt[pp[i][u]], 1);
                 }
@@ -647,19 +747,27 @@ k_sweep_cold(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__rest
 template <int DT, int K>
 __global__ void __launch_bounds__(SW_TPB, 1)
 k_sweep_acc(const int32_t *__restrict__ pkeys, const typename Fmt<DT>::V *__restrict__ pvals,
-            const int64_t *__restrict__ items, int32_t *ctrl, int32_t G, int gbits, int32_t *__restrict__ kglob,
-            unsigned long long *__restrict__ slots, uint32_t *__restrict__ status) {
+            const int64_t *__restrict__ items, const int32_t *__restrict__ bfirst, int32_t *ctrl, int32_t G,
+            int gbits, int32_t *__restrict__ kglob, unsigned long long *__restrict__ slots,
+            uint32_t *__restrict__ status) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_mm[TAB_MM];
     __shared__ int s_item;
     const int tid = threadIdx.x;
     const int Gp = 1 << gbits;
     uint32_t flags = 0;
-    for (;;) {
-        if (tid == 0) s_item = atomicAdd(&ctrl[1], 1);
-        __syncthreads();
-        const int it = s_item;
-        if (it >= ctrl[0]) break;
+    for (int k = 0;; ++k) {
+        int it;
+        if (SW_BAL) {  // this block's own items (no queue)
+            it = bfirst[blockIdx.x] + k;
+            if (it >= bfirst[blockIdx.x + 1]) break;
+            __syncthreads();  // the previous item's table is published
+        } else {
+            if (tid == 0) s_item = atomicAdd(&ctrl[1], 1);
+            __syncthreads();
+            it = s_item;
+            if (it >= ctrl[0]) break;
+        }
         const int p = (int)items[3 * it];
         const int64_t r0 = items[3 * it + 1], r1 = items[3 * it + 2];
         Table<DT, K, SW_TPB, 0, false, 1> tab(smem, s_mm, min(Gp, G - p * Gp), (int64_t)p * Gp, kglob, slots);
@@ -735,7 +843,8 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
     if (sm_hot > (size_t)device_props().smem_optin - 1024) return -1;
     SwWs w = sw_carve<DT, K>(ws, n, G, pl);
     if (w.bytes > ws_bytes) return -1;
-    static thread_local size_t conf_h = 0, conf_c = 0, conf_c64 = 0, conf_a = 0;
+    static thread_local size_t conf_h = 0, conf_c[2][2] = {}, conf_a = 0;
+    const bool mr = pl.P <= SW_MRANK;  // scatter ranks by warp match
     auto conf = [](auto kern, size_t &have, size_t want) {
         if (have >= want) return true;
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)want) != cudaSuccess)
@@ -743,8 +852,19 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
         have = want;
         return true;
     };
-    if (!conf(k_sweep_hot<DT, K>, conf_h, sm_hot) || !(d32 ? conf(k_sweep_cold<DT, uint32_t>, conf_c, sm_cold) : conf(k_sweep_cold<DT, unsigned long long>, conf_c64, sm_cold)) ||
-        !conf(k_sweep_acc<DT, K>, conf_a, sm_tab))
+    // the scatter instantiation for (destination width, rank mode)
+    auto with_cold = [&](auto &&fn) {
+        if (d32) {
+            if (mr) fn(k_sweep_cold<DT, uint32_t, true>, conf_c[0][1]);
+            else fn(k_sweep_cold<DT, uint32_t, false>, conf_c[0][0]);
+        } else {
+            if (mr) fn(k_sweep_cold<DT, unsigned long long, true>, conf_c[1][1]);
+            else fn(k_sweep_cold<DT, unsigned long long, false>, conf_c[1][0]);
+        }
+    };
+    bool cold_ok = false;
+    with_cold([&](auto kern, size_t &have) { cold_ok = conf(kern, have, sm_cold); });
+    if (!conf(k_sweep_hot<DT, K>, conf_h, sm_hot) || !cold_ok || !conf(k_sweep_acc<DT, K>, conf_a, sm_tab))
         return -2;
     if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return -2;
     int rc = 0;
@@ -767,23 +887,20 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
         });
         if (rc) return rc;
         rc = traced("sweep_scan", st, launches, [&] {
-            k_sw_scan<<<1, 1024, 0, st>>>(w.cnt, pl.cgrid, pl.P, w.pstart, w.pkeys, w.items, w.ctrl);
+            k_sw_scan<<<1, 1024, 0, st>>>(w.cnt, pl.cgrid, pl.P, w.pstart, w.pkeys, w.items, w.bfirst, pl.grid,
+                                          w.ctrl);
         });
         if (rc) return rc;
         rc = traced("sweep_scatter", st, launches, [&] {
-            if (d32)
-                k_sweep_cold<DT, uint32_t><<<pl.cgrid, SW_STPB, sm_cold, st>>>(
-                    keys, (const V *)vals, n, w.bkeys, (const V *)w.bvals, G, pl.gbits, pl.P, w.cnt, w.pkeys,
-                    (V *)w.pvals, w.ctrl, cs);
-            else
-                k_sweep_cold<DT, unsigned long long><<<pl.cgrid, SW_STPB, sm_cold, st>>>(
-                    keys, (const V *)vals, n, w.bkeys, (const V *)w.bvals, G, pl.gbits, pl.P, w.cnt, w.pkeys,
-                    (V *)w.pvals, w.ctrl, cs);
+            with_cold([&](auto kern, size_t &) {
+                kern<<<pl.cgrid, SW_STPB, sm_cold, st>>>(keys, (const V *)vals, n, w.bkeys, (const V *)w.bvals, G,
+                                                         pl.gbits, pl.P, w.cnt, w.pkeys, (V *)w.pvals, w.ctrl, cs);
+            });
         });
         if (rc) return rc;
         rc = traced("sweep_accumulate", st, launches, [&] {
             k_sweep_acc<DT, K><<<device_props().sms, SW_TPB, sm_tab, st>>>(
-                w.pkeys, (const V *)w.pvals, w.items, w.ctrl, G, pl.gbits, w.kglob, w.slots, status);
+                w.pkeys, (const V *)w.pvals, w.items, w.bfirst, w.ctrl, G, pl.gbits, w.kglob, w.slots, status);
         });
         if (rc) return rc;
     }

@@ -163,3 +163,27 @@ def test_hot_partition_pass_unaligned(R, offset):
     assert rc == O.OK
     assert out.cpu().numpy().view(np.uint32).tobytes() == ref.view(np.uint32).tobytes()
     assert R.last_path() == 1
+
+
+@pytest.mark.parametrize("dtype,K", [(np.float64, 3), (np.float32, 2)])
+@pytest.mark.parametrize("layout", ["sparse_parts", "one_big_many_tiny", "few_parts"])
+def test_sweep_accumulate_schedule(R, dtype, K, layout):
+    # the accumulate blocks' row ranges are cut on a cost scale (rows + one
+    # table publish per partition): empty partitions, partitions of a few
+    # rows next to one holding most rows, and cuts that snap to partition
+    # starts all have to cover every row exactly once
+    rng = np.random.default_rng(len(layout) * 10 + K)
+    G = 1 << 20
+    n = (1 << 21) + 13
+    if layout == "sparse_parts":  # 5 partitions in use, the rest empty
+        bases = np.array([0, 300000, 500000, 777777, G - 9])
+        keys = bases[rng.integers(0, 5, n)] + rng.integers(0, 8, n)
+    elif layout == "one_big_many_tiny":  # ~90% in one partition, 1-3 rows in many others
+        keys = rng.integers(20000, 24000, n)
+        tiny = rng.random(n) < 0.1
+        keys[tiny] = rng.integers(0, G, int(tiny.sum()))
+    else:  # uniform over 3 partitions' worth of groups, offset
+        keys = rng.integers(9000, 9000 + 3 * 8192, n)
+    keys = np.minimum(keys, G - 1).astype(np.int32)
+    vals = (rng.standard_normal(n) * np.exp2(rng.integers(-12, 12, n))).astype(dtype)
+    run(R, keys, vals, G, K)

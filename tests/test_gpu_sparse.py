@@ -39,6 +39,23 @@ def test_sparse_matches_oracle(R, dtype, distinct, n, K):
     assert torch.equal(uk, uk2) and torch.equal(out, out2)
 
 
+@pytest.mark.parametrize("lo,distinct", [(-2500, 5000), (1 << 40, 70000), (-(1 << 62), 3)])
+def test_sparse_dense_key_runs(R, lo, distinct):
+    # consecutive keys share their high digits: every radix pass but the low
+    # ones sees long runs of equal digits (stability decides the order)
+    rng = np.random.default_rng(distinct)
+    n = 8 * distinct + 11
+    keys = (lo + rng.integers(0, distinct, n)).astype(np.int64)
+    keys[:distinct] = lo + np.arange(distinct)  # every key present
+    vals = (rng.standard_normal(n) * 2.0 ** rng.integers(-20, 20, n)).astype(np.float64)
+    uk, out = R.groupby_sum_sparse(dev(keys), dev(vals), max_groups=distinct + 7, fold=3)
+    rc, ruk, rout = O.groupby_sum_sparse(keys, vals, 3)
+    assert rc == O.OK
+    assert np.array_equal(uk.cpu().numpy(), ruk)
+    assert np.array_equal(ruk, lo + np.arange(distinct))
+    assert out.cpu().numpy().tobytes() == rout.tobytes()
+
+
 def test_sparse_capacity_and_errors(R):
     keys = np.arange(5000, dtype=np.int64) * 7919
     vals = np.ones(5000)
