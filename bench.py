@@ -153,12 +153,15 @@ def fp_add_rate(R, dt):
     return _FP_RATE[dt]
 
 
-def ncu_traffic(config):
+def ncu_traffic(config, G, n, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture of this exact
+    workload and launch size (profiles/ncu_traffic.json "r2"); (None, None) when none matches."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            return json.load(fh).get(f"config{config}")
+            e = json.load(fh).get("r2", {}).get(f"config{config}:G{G}:n{n}:{kernel}")
+        return (e["traffic"], e["source"]) if e else (None, None)
     except Exception:
-        return None
+        return None, None
 
 
 class ClockSampler:
@@ -511,11 +514,14 @@ def run_workload(R, torch, args, config, n, G, K, dts, world, rank, local, steps
         avg_ms = kms / cnt
         alg_bytes = n * row_bytes  # the kernel's algorithmic input bytes per launch
         achieved = alg_bytes / (avg_ms * 1e-3) / 1e9
+        traffic, traffic_src = ncu_traffic(config, G, n, name)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": name, "kernel_ms": avg_ms,
+                "traffic": traffic, "kernel": name, "kernel_ms": avg_ms,
                 "kernel_share_of_step": kms / ms_b if ms_b else None, "alg_bytes_per_launch": alg_bytes,
                 "alg_bytes_per_row": row_bytes, "peak_source": peak_src,
-                "traffic_note": "DRAM bytes per launch from ncu --set full: profiles/r2_*_ncu_full.txt"}
+                "traffic_note": ("dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu --set full capture "
+                                 "of this workload: " + traffic_src) if traffic_src else
+                "no ncu --set full capture of this kernel at this launch size (profiles/r2_*_ncu_full.txt)"}
     if roof is not None:
         # FP side of the roofline: 3K - 2 correctly rounded
         # adds per deposited value at the MEASURED add rate of this GPU
