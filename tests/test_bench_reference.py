@@ -32,3 +32,19 @@ def test_reference_arm_prints_the_contract_line(config):
     assert d["repo_libs_mapped"] is not None
     assert not any("librepro_b200" in p for p in d["repo_libs_mapped"]), d["repo_libs_mapped"]
     assert any("liboracle" in p for p in d["repo_libs_mapped"]), d["repo_libs_mapped"]
+
+
+def test_roofline_traffic_lookup_matches_workload_launch_and_kernel():
+    """roofline.traffic comes from a committed ncu --set full capture only when config, group count, launch size and
+    kernel all match; every source it names is a tracked profile holding the dram__bytes metrics."""
+    sys.path.insert(0, ROOT)
+    import bench
+    t, src = bench.ncu_traffic(1, 1024, 1 << 27, "table_accumulate")
+    assert t and 1.0 <= t / ((1 << 27) * 12) < 1.05 and os.path.exists(os.path.join(ROOT, src))
+    assert bench.ncu_traffic(1, 1024, 1 << 26, "table_accumulate") == (None, None)
+    assert bench.ncu_traffic(1, 1024, 1 << 27, "fold") == (None, None)
+    with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+        for key, e in json.load(fh)["r2"].items():
+            with open(os.path.join(ROOT, e["source"])) as ph:
+                text = ph.read()
+            assert "dram__bytes_read.sum" in text and "dram__bytes_write.sum" in text, key
