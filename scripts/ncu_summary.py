@@ -7,6 +7,7 @@ rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
 h = rows[0]
+units = dict(zip(h, rows[1]))
 for v in rows[2:]:
     d = dict(zip(h, v))
     print("kernel:", d.get("Kernel Name", "")[:90])
@@ -19,7 +20,7 @@ for v in rows[2:]:
             "smsp__inst_executed_op_shared_atom.sum", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
             "launch__registers_per_thread", "launch__grid_size", "launch__occupancy_limit_registers"]
     for k in keys:
-        print(f"  {k:75s} {d.get(k)}")
+        print(f"  {k:75s} {d.get(k)} {units.get(k, '')}")
     st = {k: d[k] for k in h if k.startswith("smsp__pcsamp_warps_issue_stalled") and "not_issued" not in k}
     tot = sum(float(x.replace(",", "") or 0) for x in st.values()) or 1
     for k, x in sorted(st.items(), key=lambda kv: -float(kv[1].replace(",", "") or 0))[:10]:
