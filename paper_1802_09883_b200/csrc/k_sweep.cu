@@ -38,6 +38,7 @@
 #include "table_core.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace repro {
 
@@ -69,6 +70,11 @@ constexpr int SW_HTPB = 512;           // hot-partition pass (one block per SM: 
 #ifndef SW_MRANK
 #define SW_MRANK 8    // scatter ranks by warp match + one atomic per distinct partition up to this many partitions
 #endif                // (P = 4: 1.744 -> 1.542 ms; P = 16: 1.617 -> 1.743; P = 256: 2.30 -> 3.07 -- one atomic per row)
+#ifndef SW_REP_MAXP
+#define SW_REP_MAXP 3  // plans of 2 .. SW_REP_MAXP partitions take the replicated-read form (k_sweep_hot<REP>):
+                       // 2^28 rows, scatter form -> replicated: binary64 K=3 P=2 2.67 -> 1.80 ms, P=3 2.67 -> 2.57, P=4 2.68 -> 3.39;
+                       // binary32 K=2 P=2 2.15 -> 1.18, P=3 2.19 -> 1.71; binary64 K=2 P=3 2.52 -> 2.07
+#endif
 #ifndef SW_CBPS64
 #define SW_CBPS64 2   // scatter blocks per SM, binary64 (shared memory: stage + carry)
 #endif
@@ -270,24 +276,29 @@ __global__ void __launch_bounds__(1024) k_sw_sample(const int32_t *__restrict__ 
 // away (the heavy partition never goes back to HBM) and compacts the other
 // rows, coalesced per warp, into a contiguous buffer for 3-5.  Exits at once
 // when there is no hot partition.
-template <int DT, int K>
+// REP > 0 (the replicated-read form for plans of 2 .. SW_REP_MAXP partitions):
+// no sample, no scatter -- block b streams row chunk b / REP_P and deposits the
+// rows of partition b % REP_P only (the others add zeros to the sink columns),
+// so the REP_P blocks of one chunk read the same rows at the same pace (the
+// later readers hit L2) and nothing is written back to HBM.
+template <int DT, int K, bool REP = false>
 __global__ void __launch_bounds__(SW_HTPB, 1)
 k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restrict__ vals, int64_t n, int32_t G,
             int gbits, int64_t chunk, int32_t *__restrict__ bkeys, typename Fmt<DT>::V *__restrict__ bvals,
             int32_t *__restrict__ ctrl, int64_t *__restrict__ hcnt, int32_t *__restrict__ kglob,
-            unsigned long long *__restrict__ slots, uint32_t *__restrict__ status) {
+            unsigned long long *__restrict__ slots, uint32_t *__restrict__ status, int rep_p) {
     using V = typename Fmt<DT>::V;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_mm[TAB_MM];
     __shared__ int s_ccount;  // cold rows compacted by this block (its region starts at row0)
-    const int hot = ctrl[3];
+    const int hot = REP ? (int)(blockIdx.x % rep_p) : ctrl[3];
     if (hot < 0) return;
     const int tid = threadIdx.x, lane = tid & 31;
     const int Gp = 1 << gbits;
-    const int64_t row0 = (int64_t)blockIdx.x * chunk;
+    const int64_t row0 = (int64_t)(REP ? blockIdx.x / rep_p : blockIdx.x) * chunk;
     const int64_t row1 = min(n, row0 + chunk);
     if (row0 >= row1) return;
-    const int nh = min(ctrl[5], TAB_HMAX);
+    const int nh = REP ? 0 : min(ctrl[5], TAB_HMAX);
     Table<DT, K, SW_HTPB, 0, true, 1> tab(smem, s_mm, min(Gp, G - hot * Gp), (int64_t)hot * Gp, kglob, slots, nh);
     tab.clear();
     if (tid == 0) s_ccount = 0;
@@ -308,7 +319,7 @@ k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restr
             const bool ok = (uint32_t)k < (uint32_t)G;
             const bool h = ok && (k >> gbits) == hot;
             hin |= (iu && h) ? 1u << u : 0u;
-            cin |= (iu && ok && !h) ? 1u << u : 0u;
+            cin |= (!REP && iu && ok && !h) ? 1u << u : 0u;
             bad |= (iu && !ok) ? 1u : 0u;
             hk[u] = k & (Gp - 1);
         }
@@ -316,14 +327,16 @@ k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restr
         // compaction: one ballot per quad slot; the warp's cold rows of slot u
         // land in consecutive positions (coalesced stores), one shared atomic
         // per warp reserves them in the block's region
-        uint32_t m[4];
+        uint32_t m[4] = {0, 0, 0, 0};
         int tot = 0;
+        if (!REP) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            m[u] = __ballot_sync(0xffffffffu, (cin >> u) & 1u);
-            tot += __popc(m[u]);
+            for (int u = 0; u < 4; ++u) {
+                m[u] = __ballot_sync(0xffffffffu, (cin >> u) & 1u);
+                tot += __popc(m[u]);
+            }
         }
-        if (tot) {  // (warp-uniform)
+        if (!REP && tot) {  // (warp-uniform)
             int base = 0;
             if (lane == 0) base = atomicAdd(&s_ccount, tot);
             base = __shfl_sync(0xffffffffu, base, 0);
@@ -371,7 +384,7 @@ k_sweep_hot(const int32_t *__restrict__ keys, const typename Fmt<DT>::V *__restr
         step(t, tid == 0 ? (1u << tail) - 1u : 0u);
     }
     tab.finish();  // (barriers on both sides: every warp's compaction is done)
-    if (tid == 0) hcnt[blockIdx.x] = s_ccount;
+    if (!REP && tid == 0) hcnt[blockIdx.x] = s_ccount;
     flags = __reduce_or_sync(0xffffffffu, flags);
     if (lane == 0 && flags) atomicOr(status, flags);
 }
@@ -825,6 +838,13 @@ k_sweep_acc(const int32_t *__restrict__ pkeys, const typename Fmt<DT>::V *__rest
     if ((tid & 31) == 0 && flags) atomicOr(status, flags);
 }
 
+// largest plan (partitions) that takes the replicated-read form; REPRO_SWEEP_REP_MAXP overrides (0 / 1: off)
+int sweep_rep_maxp() {
+    const char *e = getenv("REPRO_SWEEP_REP_MAXP");
+    if (e && *e) return atoi(e);
+    return SW_REP_MAXP;
+}
+
 template <int DT, int K>
 int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, void *ws, size_t ws_bytes,
                    int merge, int32_t *acc_k, int64_t *acc_C, int64_t *acc_D, void *out, uint32_t *status,
@@ -868,7 +888,22 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
         return -2;
     if (cudaMemsetAsync(ws, 0, w.zero_bytes, st) != cudaSuccess) return -2;
     int rc = 0;
-    if (n > 0) {
+    const int rep_max = sweep_rep_maxp();
+    if (n > 0 && pl.P >= 2 && pl.P <= rep_max && pl.P <= pl.grid) {
+        // replicated-read form: P blocks per row chunk, one partition each; no scatter
+        static thread_local size_t conf_r = 0;
+        if (!conf(k_sweep_hot<DT, K, true>, conf_r, sm_hot)) return -2;
+        const int chunks = pl.grid / pl.P;
+        int64_t chunk = (n + chunks - 1) / chunks;
+        chunk = (chunk + 3) & ~(int64_t)3;
+        const int grid = (int)((n + chunk - 1) / chunk) * pl.P;
+        rc = traced("sweep_replicated", st, launches, [&] {
+            k_sweep_hot<DT, K, true><<<grid, SW_HTPB, sm_hot, st>>>(keys, (const V *)vals, n, G, pl.gbits, chunk,
+                                                                   w.bkeys, (V *)w.bvals, w.ctrl, w.hcnt, w.kglob,
+                                                                   w.slots, status, pl.P);
+        });
+        if (rc) return rc;
+    } else if (n > 0) {
         rc = traced("sweep_sample", st, launches, [&] {
             k_sw_sample<<<1, 1024, 0, st>>>(keys, n, G, pl.gbits, pl.P, w.ctrl);
         });
@@ -879,7 +914,7 @@ int launch_sweep_t(const int32_t *keys, const void *vals, int64_t n, int32_t G, 
         const ColdSrc cs{w.hcnt, grid, chunk};
         rc = traced("sweep_hot", st, launches, [&] {  // returns at once when no partition is hot
             k_sweep_hot<DT, K><<<grid, SW_HTPB, sm_hot, st>>>(keys, (const V *)vals, n, G, pl.gbits, chunk, w.bkeys,
-                                                             (V *)w.bvals, w.ctrl, w.hcnt, w.kglob, w.slots, status);
+                                                             (V *)w.bvals, w.ctrl, w.hcnt, w.kglob, w.slots, status, 1);
         });
         if (rc) return rc;
         rc = traced("sweep_hist", st, launches, [&] {

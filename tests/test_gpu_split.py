@@ -33,7 +33,8 @@ def rows(G, n, dtype, seed):
 
 @pytest.mark.parametrize("world", [1, 2, 3, 8])
 @pytest.mark.parametrize("G,dtype,K", [(1024, np.float64, 3), (16, np.float32, 2), (50000, np.float64, 3),
-                                       (70000, np.float32, 2)])
+                                       (70000, np.float32, 2),
+                                       (8000, np.float64, 3), (16000, np.float32, 2)])  # (2-partition plans: replicated-read form)
 def test_split_form_emulated_ranks(R, world, G, dtype, K):
     n = 300007
     keys, vals = rows(G, n, dtype, world + G)
