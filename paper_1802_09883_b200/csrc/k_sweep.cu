@@ -24,7 +24,11 @@
 //                   completed in L2 before write-back.
 //   6. k_sweep_acc  persistent blocks pull work items (row ranges of one
 //                   partition) and run the on-chip table over them.
-// Both tables publish into the absolute-level slot table (kglob, slots) that
+// Plans of 2 .. SW_REP_MAXP partitions skip 1-6 for the REPLICATED-READ form
+// (k_sweep_hot<REP>): P blocks stream each row chunk at the same pace, each
+// depositing one partition's rows on chip; the later readers hit L2, so HBM
+// sees the rows once (12 B per binary64 row) and nothing is written back.
+// All tables publish into the absolute-level slot table (kglob, slots) that
 // k_fold (k_state.cu) turns into canonical states and Eq. 1 read-outs.  Each
 // group lives in exactly one partition; the order of rows inside a partition
 // is irrelevant (the accumulator is associative).
