@@ -111,3 +111,21 @@ def test_replicated_read_unaligned(R, maxp):
     rc, ref = O.groupby_sum(keys, vals, G, 3)
     assert rc == O.OK
     assert out.cpu().numpy().view(np.uint64).tobytes() == ref.view(np.uint64).tobytes()
+
+
+def test_replicated_read_host_entry_and_chunked_handle(R, maxp):
+    # the host entry point (H2D chunks pipelined with deposits) and the handle API (deposits merged into a
+    # canonical state) go through the same form; state and sums equal the oracle's
+    rng = np.random.default_rng(9)
+    G, n = 8000, (1 << 21) + 11
+    keys = rng.integers(0, G, n).astype(np.int32)
+    vals = values(rng, n, np.float64, -30, 60)
+    rc, ref, st = O.groupby_sum(keys, vals, G, 3, with_state=True)
+    assert rc == O.OK
+    got = R.groupby_sum_host(torch.from_numpy(keys).pin_memory(), torch.from_numpy(vals).pin_memory(), G, 3).numpy()
+    assert got.view(np.uint64).tobytes() == ref.view(np.uint64).tobytes()
+    a = R.Accumulator(G, 3, R.F64)
+    for c0, c1 in ((0, 5), (5, 1 << 20), (1 << 20, n)):
+        a.deposit(torch.from_numpy(keys[c0:c1]).cuda(), torch.from_numpy(vals[c0:c1]).cuda())
+    assert a.finalize().cpu().numpy().view(np.uint64).tobytes() == ref.view(np.uint64).tobytes()
+    assert a.export().cpu().numpy().reshape(G, 6).tobytes() == st.tobytes()
